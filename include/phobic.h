@@ -1,0 +1,163 @@
+/*
+ * phobic.h — C-ABI of the B200-native PHOBIC construction engine
+ * (libphobic_b200.so, built from paper_2404_18497_b200/csrc/).
+ *
+ * Conventions (mirroring the reference operator layer, pilothash._kernels,
+ * /root/reference/pkg/src/pilothash/_kernels.py:1-9):
+ *   - every pointer argument is a DEVICE pointer (cudaMalloc / torch CUDA
+ *     memory) unless documented as host memory;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - the caller allocates and, where the reference zero-fills
+ *     (builder.py:238-240), zero-fills every output; kernels write in place
+ *     and keep no allocation across calls;
+ *   - every function returns 0 on success, a cudaError_t value (1..999) for
+ *     CUDA / launch errors, or one of the PHB_E_* codes below. Per-partition
+ *     search failures are DATA (status_out), exactly as in the reference.
+ *
+ * Key ABI: a 64-bit key is its 8-byte little-endian string (SURVEY.md §0
+ * finding 4); byte keys are a flat buffer plus int64 offsets[n+1]
+ * (keygen.KeyCorpus, keygen.py:25-57).
+ */
+#ifndef PHOBIC_B200_H
+#define PHOBIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PHB_OK 0
+#define PHB_E_BUCKETS 1001             /* bucket count outside [1, 65535] */
+#define PHB_E_PARTITION_TOO_LARGE 1002 /* a partition's search state exceeds shared memory */
+#define PHB_E_ARGS 1003                /* invalid sizes / misaligned buffers */
+
+const char* phb_version(void);
+const char* phb_error_string(int code);
+int phb_device_sms(void);
+
+/* ---------------------------------------------------------------------
+ * Reference-shaped operators: one-for-one replacements of the three
+ * pilothash._kernels entry points (same argument meaning and layout).
+ * ------------------------------------------------------------------- */
+
+/* replaces _kernels.murmur3_many(buf, offsets, seed, out_hi, out_lo)
+ * (_kernels.py:89-146), called by hashing.master_hash_many (hashing.py:65-76).
+ * offsets has n+1 entries. */
+int phb_murmur3_many(const uint8_t* buf, const int64_t* offsets, int64_t n, uint64_t seed,
+                     uint64_t* out_hi, uint64_t* out_lo, void* stream);
+
+/* u64 fast path of the same hash: keys[i] hashed as its 8-byte LE string. */
+int phb_murmur3_u64(const uint64_t* keys, int64_t n, uint64_t seed, uint64_t* out_hi,
+                    uint64_t* out_lo, void* stream);
+
+/* replaces _kernels.build_partition_range(his, los, key_off, p_lo, p_hi,
+ * entries, bcount, seed_cap, tie_desc, seeds_out, trials_out, status_out)
+ * (_kernels.py:221-371), called by builder.build_all_partitions
+ * (builder.py:244-258). Keys must arrive grouped by partition (any order
+ * inside a partition). entries: the 2049 f64 table built on the host
+ * (assignment.tabulate, assignment.py:115-121). tie_desc follows the
+ * reference flag (1 for "asc-expected", builder.py:241). Outputs:
+ * seeds_out[j*bcount + b-1] (u64), trials_out (i64, same index, may be
+ * NULL), status_out[j] (0 ok, 1 duplicate low words, 2 seed cap). */
+int phb_build_partition_range(const uint64_t* his, const uint64_t* los, const int64_t* key_off,
+                              int64_t p_lo, int64_t p_hi, const double* entries, int32_t bcount,
+                              int64_t seed_cap, int32_t tie_desc, uint64_t* seeds_out,
+                              int64_t* trials_out, uint8_t* status_out, void* stream);
+
+/* replaces _kernels.query_many_kernel(his, los, n, nparts, deltas, entries,
+ * bcount, seed_mat, out) (_kernels.py:379-397), called by Mphf.query_many
+ * (mphf.py:130-145). seed_mat is row-major [nparts, bcount] u64. */
+int phb_query_many(const uint64_t* his, const uint64_t* los, int64_t nq, int64_t n,
+                   int64_t nparts, const int64_t* deltas, const double* entries, int32_t bcount,
+                   const uint64_t* seed_mat, int64_t* out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Staged build pipeline (what pilothash.mphf.build, mphf.py:236-290,
+ * becomes on B200). keys64 != NULL selects the u64 path, otherwise
+ * (buf, offsets) byte keys.
+ * ------------------------------------------------------------------- */
+
+/* K1: murmur3 + partition index + per-partition counts (counts zeroed by
+ * caller). Replaces master_hash_many + partition_index_many + bincount
+ * (partitioning.py:73-96). */
+int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
+                   uint64_t seed, int64_t nparts, uint32_t* counts, void* stream);
+
+/* K2: counts[nparts] -> key_off[nparts+1] (local, from 0) and
+ * deltas[nparts+1] = key_base + key_off[j] - expected(part_base + j,
+ * global_n, global_nparts) (partitioning.py:101-108); stats[0] = max |delta|,
+ * stats[1] = max partition size. For a single-GPU build pass key_base =
+ * part_base = 0, global_n = n, global_nparts = nparts. */
+int phb_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
+               int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
+               int64_t* stats, void* stream);
+
+/* K3: re-hash and scatter (lo, bucket id) into partition ranges (cursor[]
+ * zeroed by caller). Replaces the lexsort grouping (partitioning.py:93-95)
+ * and _bucket_of (_kernels.py:252-255). */
+int phb_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
+                uint64_t seed, int64_t nparts, const double* entries, int32_t bcount,
+                const int64_t* key_off, uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
+                void* stream);
+
+/* K4: bucket order + seed search for partitions [p_lo, p_hi) over records
+ * grouped by partition. Seeds land at seeds[(j-out_base)*s_sj + (b-1)*s_sb];
+ * trials (may be NULL) at the same index; part_trials[(j-out_base)] (may be
+ * NULL); status[(j-out_base)]. glo: scratch indexed like lo. queue: one
+ * device u32. m_max: largest partition size in the range (layout stats[1]). */
+int phb_search(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off, int64_t p_lo,
+               int64_t p_hi, int64_t out_base, int32_t bcount, int64_t seed_cap, int32_t tie_desc,
+               int64_t m_max, uint64_t* seeds, int64_t s_sj, int64_t s_sb, int64_t* trials,
+               int64_t* part_trials, uint8_t* status, uint64_t* glo, uint32_t* queue,
+               void* stream);
+
+/* K5/K6: interleaved / mono Compact-Rice encoding of a column-major seed
+ * matrix seeds[bcount][nparts] plus the packed deltas, into the serialized
+ * body of Mphf.serialize (mphf.py:156-175) from byte 57 on (the fixed header
+ * and the blake2b checksum are host work). Two phases: plan (sizes; writes
+ * 8 int64 to HOST summary_out: total_bytes, seed_section, trials_total,
+ * first_bad, bad_code, delta_width, ncols, 0; synchronizes `stream`) and
+ * write (blob: device, 4-byte aligned, >= total_bytes + 16 bytes). */
+size_t phb_encode_workspace_bytes(int64_t nparts, int32_t bcount, int32_t mono);
+int phb_encode_plan(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                    int32_t compact_prefix, const int64_t* deltas, int64_t nparts_global,
+                    const int64_t* layout_stats, const uint8_t* status,
+                    const int64_t* part_trials, void* workspace, int64_t* summary_out,
+                    void* stream);
+int phb_encode_write(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                     int32_t compact_prefix, const int64_t* deltas, int64_t nparts_global,
+                     const int64_t* layout_stats, void* workspace, uint8_t* blob,
+                     size_t blob_bytes, void* stream);
+
+/* Decode an encoded seed section (device copy of a serialized body) back to
+ * the column-major matrix seeds[bcount][nparts] (decode_matrix,
+ * encoders.py:309-311 / :337-338). col_info: HOST array of 8 int64 per
+ * encoder (kind, param, count, payload_byte, highs_byte, highs_nbits, 0, 0)
+ * as parsed by the host from the block headers. */
+int phb_decode_seeds(const uint8_t* blob, int64_t ncols, const int64_t* col_info, int64_t nparts,
+                     int32_t bcount, int32_t mono, uint64_t* seeds, void* stream);
+
+/* K7: batched query with fused hashing; key_off[nparts+1] absolute offsets
+ * (expected + delta). seeds indexed [j*s_sj + (b-1)*s_sb]. */
+int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t nq,
+              uint64_t seed, int64_t n, int64_t nparts, const int64_t* key_off,
+              const double* entries, int32_t bcount, const uint64_t* seeds, int64_t s_sj,
+              int64_t s_sb, int64_t* out, void* stream);
+
+/* K8: bijection check onto [0, n): bitmap (ceil(n/32) u32, zeroed by
+ * caller) and bad_flag (one u32, zeroed) set to 1 on a repeat or an
+ * out-of-range output. Bijection <=> nq == n and bad_flag == 0. */
+int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad_flag,
+               void* stream);
+
+/* key_off[j] = expected(j, n, nparts) + deltas[j], j in [0, nparts]
+ * (partitioning.offset, partitioning.py:119-122). */
+int phb_offsets_from_deltas(const int64_t* deltas, int64_t n, int64_t nparts, int64_t* key_off,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHOBIC_B200_H */

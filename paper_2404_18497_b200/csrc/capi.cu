@@ -1,0 +1,295 @@
+// extern "C" boundary of libphobic_b200.so (declared in include/phobic.h).
+// Thin argument marshalling around the launchers; no state survives a call.
+#include <algorithm>
+#include <cstdio>
+
+#include "../../include/phobic.h"
+#include "common.cuh"
+#include "phobic_encode.h"
+#include "phobic_internal.h"
+
+namespace phb {
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1)
+      v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+int launch_decode(const uint8_t* blob, int64_t ncols, const int64_t* host_info, int64_t nparts,
+                  uint32_t B, int mono, uint64_t* seeds, cudaStream_t st);
+
+__global__ void k_range_max(const int64_t* __restrict__ key_off, int64_t p_lo, int64_t p_hi,
+                            unsigned long long* __restrict__ out) {
+  unsigned long long mx = 0;
+  for (int64_t j = p_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < p_hi;
+       j += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, (unsigned long long)(key_off[j + 1] - key_off[j]));
+  atomicMax(out, mx);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[1] = (unsigned long long)key_off[p_lo];
+    out[2] = (unsigned long long)key_off[p_hi];
+  }
+}
+
+__global__ void k_offsets_from_deltas(const int64_t* __restrict__ deltas, int64_t n,
+                                      int64_t nparts, int64_t* __restrict__ key_off) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= nparts;
+       j += (int64_t)gridDim.x * blockDim.x)
+    key_off[j] = expected_offset(j, n, nparts) + deltas[j];
+}
+
+}  // namespace phb
+
+using namespace phb;
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+const char* phb_version(void) { return "phobic-b200 0.1.0 (sm_100a)"; }
+
+const char* phb_error_string(int code) {
+  switch (code) {
+    case PHB_OK:
+      return "ok";
+    case PHB_E_BUCKETS:
+      return "bucket count outside [1, 65535]";
+    case PHB_E_PARTITION_TOO_LARGE:
+      return "partition search state exceeds shared memory";
+    case PHB_E_ARGS:
+      return "invalid arguments";
+    default:
+      if (code > 0 && code < 1000) return cudaGetErrorString((cudaError_t)code);
+      return "unknown error";
+  }
+}
+
+int phb_device_sms(void) { return num_sms(); }
+
+int phb_murmur3_many(const uint8_t* buf, const int64_t* offsets, int64_t n, uint64_t seed,
+                     uint64_t* out_hi, uint64_t* out_lo, void* stream) {
+  if (n < 0 || (n > 0 && !offsets)) return PHB_E_ARGS;
+  return launch_murmur(buf, offsets, nullptr, n, seed, out_hi, out_lo, S(stream));
+}
+
+int phb_murmur3_u64(const uint64_t* keys, int64_t n, uint64_t seed, uint64_t* out_hi,
+                    uint64_t* out_lo, void* stream) {
+  if (n < 0 || (n > 0 && !keys)) return PHB_E_ARGS;
+  return launch_murmur(nullptr, nullptr, keys, n, seed, out_hi, out_lo, S(stream));
+}
+
+int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
+                   uint64_t seed, int64_t nparts, uint32_t* counts, void* stream) {
+  if (n < 0 || nparts < 1 || nparts >= (int64_t(1) << 32)) return PHB_E_ARGS;
+  return launch_hash_count(buf, offsets, keys64, n, seed, (uint64_t)nparts, counts, S(stream));
+}
+
+int phb_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
+               int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
+               int64_t* stats, void* stream) {
+  return launch_layout(counts, nparts, key_base, part_base, global_n, global_nparts, key_off,
+                       deltas, stats, nullptr, 0, S(stream));
+}
+
+int phb_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
+                uint64_t seed, int64_t nparts, const double* entries, int32_t bcount,
+                const int64_t* key_off, uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
+                void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (n < 0 || nparts < 1) return PHB_E_ARGS;
+  return launch_scatter(buf, offsets, keys64, n, seed, (uint64_t)nparts, entries,
+                        (uint32_t)bcount, key_off, cursor, lo_out, bid_out, S(stream));
+}
+
+int phb_search(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off, int64_t p_lo,
+               int64_t p_hi, int64_t out_base, int32_t bcount, int64_t seed_cap, int32_t tie_desc,
+               int64_t m_max, uint64_t* seeds, int64_t s_sj, int64_t s_sb, int64_t* trials,
+               int64_t* part_trials, uint8_t* status, uint64_t* glo, uint32_t* queue,
+               void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  SearchArgs a;
+  a.lo = lo;
+  a.bid = bid;
+  a.key_off = key_off;
+  a.p_lo = p_lo;
+  a.p_hi = p_hi;
+  a.out_base = out_base;
+  a.bcount = (uint32_t)bcount;
+  a.seed_cap = seed_cap;
+  a.tie_desc = tie_desc;
+  a.seeds = seeds;
+  a.s_sj = s_sj;
+  a.s_sb = s_sb;
+  a.trials = trials;
+  a.part_trials = part_trials;
+  a.status = status;
+  a.glo = glo;
+  a.queue = queue;
+  a.m_max = m_max;
+  return launch_search(a, S(stream));
+}
+
+int phb_build_partition_range(const uint64_t* his, const uint64_t* los, const int64_t* key_off,
+                              int64_t p_lo, int64_t p_hi, const double* entries, int32_t bcount,
+                              int64_t seed_cap, int32_t tie_desc, uint64_t* seeds_out,
+                              int64_t* trials_out, uint8_t* status_out, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (p_hi <= p_lo) return 0;
+  cudaStream_t st = S(stream);
+  unsigned long long* d_stat = nullptr;
+  unsigned long long h_stat[3] = {0, 0, 0};
+  PHB_CUDA_TRY(cudaMallocAsync(&d_stat, 3 * sizeof(unsigned long long), st));
+  PHB_CUDA_TRY(cudaMemsetAsync(d_stat, 0, 3 * sizeof(unsigned long long), st));
+  int g = (int)std::min<int64_t>((p_hi - p_lo + 255) / 256, 1024);
+  k_range_max<<<g, 256, 0, st>>>(key_off, p_lo, p_hi, d_stat);
+  PHB_CUDA_TRY(cudaGetLastError());
+  PHB_CUDA_TRY(cudaMemcpyAsync(h_stat, d_stat, sizeof(h_stat), cudaMemcpyDeviceToHost, st));
+  PHB_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t k0 = (int64_t)h_stat[1], k1 = (int64_t)h_stat[2];
+  const int64_t nk = k1 - k0;
+  uint16_t* bid = nullptr;
+  uint64_t* glo = nullptr;
+  uint32_t* queue = nullptr;
+  PHB_CUDA_TRY(cudaMallocAsync(&bid, sizeof(uint16_t) * (nk > 0 ? nk : 1), st));
+  PHB_CUDA_TRY(cudaMallocAsync(&glo, sizeof(uint64_t) * (nk > 0 ? nk : 1), st));
+  PHB_CUDA_TRY(cudaMallocAsync(&queue, sizeof(uint32_t), st));
+  int rc = launch_bucket_ids(his + k0, nk, entries, (uint32_t)bcount, bid, st);
+  if (rc == 0) {
+    SearchArgs a;
+    a.lo = los;
+    a.bid = bid - k0;   // absolute indexing by key_off
+    a.key_off = key_off;
+    a.p_lo = p_lo;
+    a.p_hi = p_hi;
+    a.out_base = 0;
+    a.bcount = (uint32_t)bcount;
+    a.seed_cap = seed_cap;
+    a.tie_desc = tie_desc;
+    a.seeds = seeds_out;
+    a.s_sj = bcount;
+    a.s_sb = 1;
+    a.trials = trials_out;
+    a.part_trials = nullptr;
+    a.status = status_out;
+    a.glo = glo - k0;
+    a.queue = queue;
+    a.m_max = (int64_t)h_stat[0];
+    rc = launch_search(a, st);
+  }
+  cudaFreeAsync(bid, st);
+  cudaFreeAsync(glo, st);
+  cudaFreeAsync(queue, st);
+  cudaFreeAsync(d_stat, st);
+  return rc;
+}
+
+int phb_offsets_from_deltas(const int64_t* deltas, int64_t n, int64_t nparts, int64_t* key_off,
+                            void* stream) {
+  if (nparts < 1) return PHB_E_ARGS;
+  int g = (int)std::min<int64_t>((nparts + 256) / 256, 4096);
+  k_offsets_from_deltas<<<g, 256, 0, S(stream)>>>(deltas, n, nparts, key_off);
+  return (int)cudaGetLastError();
+}
+
+int phb_query_many(const uint64_t* his, const uint64_t* los, int64_t nq, int64_t n,
+                   int64_t nparts, const int64_t* deltas, const double* entries, int32_t bcount,
+                   const uint64_t* seed_mat, int64_t* out, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (nparts < 1) return PHB_E_ARGS;
+  cudaStream_t st = S(stream);
+  int64_t* key_off = nullptr;
+  PHB_CUDA_TRY(cudaMallocAsync(&key_off, sizeof(int64_t) * (nparts + 1), st));
+  int rc = phb_offsets_from_deltas(deltas, n, nparts, key_off, stream);
+  if (rc == 0)
+    rc = launch_query(nullptr, nullptr, nullptr, his, los, nq, 0, n, nparts, key_off, entries,
+                      (uint32_t)bcount, seed_mat, bcount, 1, out, st);
+  cudaFreeAsync(key_off, st);
+  return rc;
+}
+
+size_t phb_encode_workspace_bytes(int64_t nparts, int32_t bcount, int32_t mono) {
+  return encode_workspace_bytes(nparts, (uint32_t)bcount, mono);
+}
+
+static EncodeArgs make_enc(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                           int32_t compact_prefix, const int64_t* deltas, int64_t nparts_global,
+                           const int64_t* layout_stats, const uint8_t* status,
+                           const int64_t* part_trials) {
+  EncodeArgs a;
+  a.seeds = seeds;
+  a.nparts = nparts;
+  a.bcount = (uint32_t)bcount;
+  a.mono = mono;
+  a.compact_prefix = compact_prefix;
+  a.deltas = deltas;
+  a.nparts_global = nparts_global;
+  a.layout_stats = layout_stats;
+  a.status = status;
+  a.part_trials = part_trials;
+  return a;
+}
+
+int phb_encode_plan(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                    int32_t compact_prefix, const int64_t* deltas, int64_t nparts_global,
+                    const int64_t* layout_stats, const uint8_t* status,
+                    const int64_t* part_trials, void* workspace, int64_t* summary_out,
+                    void* stream) {
+  if (bcount < 1 || nparts < 1 || !layout_stats || !workspace) return PHB_E_ARGS;
+  EncodeArgs a = make_enc(seeds, nparts, bcount, mono, compact_prefix, deltas, nparts_global,
+                          layout_stats, status, part_trials);
+  EncodeSummary s;
+  int rc = launch_encode_plan(a, workspace, summary_out ? &s : nullptr, S(stream));
+  if (rc == 0 && summary_out) {
+    summary_out[0] = (int64_t)s.total_bytes;
+    summary_out[1] = (int64_t)s.seed_section;
+    summary_out[2] = (int64_t)s.trials_total;
+    summary_out[3] = s.first_bad;
+    summary_out[4] = s.bad_code;
+    summary_out[5] = s.delta_width;
+    summary_out[6] = s.ncols;
+    summary_out[7] = 0;
+  }
+  return rc;
+}
+
+int phb_encode_write(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                     int32_t compact_prefix, const int64_t* deltas, int64_t nparts_global,
+                     const int64_t* layout_stats, void* workspace, uint8_t* blob,
+                     size_t blob_bytes, void* stream) {
+  if (bcount < 1 || nparts < 1 || !workspace || !blob) return PHB_E_ARGS;
+  EncodeArgs a = make_enc(seeds, nparts, bcount, mono, compact_prefix, deltas, nparts_global,
+                          layout_stats, nullptr, nullptr);
+  return launch_encode_write(a, workspace, blob, blob_bytes, S(stream));
+}
+
+int phb_decode_seeds(const uint8_t* blob, int64_t ncols, const int64_t* col_info, int64_t nparts,
+                     int32_t bcount, int32_t mono, uint64_t* seeds, void* stream) {
+  if (bcount < 1 || nparts < 1 || !col_info) return PHB_E_ARGS;
+  return launch_decode(blob, ncols, col_info, nparts, (uint32_t)bcount, mono, seeds, S(stream));
+}
+
+int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t nq,
+              uint64_t seed, int64_t n, int64_t nparts, const int64_t* key_off,
+              const double* entries, int32_t bcount, const uint64_t* seeds, int64_t s_sj,
+              int64_t s_sb, int64_t* out, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (nparts < 1) return PHB_E_ARGS;
+  return launch_query(buf, offsets, keys64, nullptr, nullptr, nq, seed, n, nparts, key_off,
+                      entries, (uint32_t)bcount, seeds, s_sj, s_sb, out, S(stream));
+}
+
+int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad_flag,
+               void* stream) {
+  return launch_verify(out, nq, n, bitmap, bad_flag, S(stream));
+}
+
+}  // extern "C"

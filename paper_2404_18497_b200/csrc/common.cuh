@@ -1,0 +1,181 @@
+// Shared device primitives for the PHOBIC construction engine (sm_100a).
+//
+// Every function here restates one arithmetic step of the reference
+// (`pilothash`, /root/reference/pkg/src/pilothash) bit for bit:
+//   mix64            _kernels.py:40-47   (splitmix64 finalizer)
+//   mulhi            _kernels.py:50-55   (exact floor(z*m / 2^64), m < 2^32)
+//   fmix64 / rotl    _kernels.py:58-70
+//   murmur3 u64/bytes _kernels.py:89-146 (canonical MurmurHash3_x64_128)
+//   bucket_of        _kernels.py:149-167 (FP64, separately rounded, no FMA)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace phb {
+
+constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
+constexpr uint64_t BUCKET_SALT = 0xC2B2AE3D27D4EB4Full;    // _kernels.py:29
+constexpr uint64_t POSITION_SALT = 0x9E3779B97F4A7C15ull;  // _kernels.py:30
+constexpr uint64_t MM_C1 = 0x87C37B91114253D5ull;
+constexpr uint64_t MM_C2 = 0x4CF5AD432745937Full;
+constexpr uint64_t MM_F1 = 0xFF51AFD7ED558CCDull;
+constexpr uint64_t MM_F2 = 0xC4CEB9FE1A85EC53ull;
+constexpr int GRID = 2048;  // assignment.py:26
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= MIX1;
+  z ^= z >> 27;
+  z *= MIX2;
+  z ^= z >> 31;
+  return z;
+}
+
+__device__ __forceinline__ uint64_t mulhi(uint64_t z, uint64_t m) { return __umul64hi(z, m); }
+
+__host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
+  return (x << r) | (x >> (64 - r));
+}
+
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+  z ^= z >> 33;
+  z *= MM_F1;
+  z ^= z >> 33;
+  z *= MM_F2;
+  z ^= z >> 33;
+  return z;
+}
+
+struct Hash128 {
+  uint64_t hi, lo;
+};
+
+// murmur3 finalisation shared by both key paths (_kernels.py:137-146).
+__device__ __forceinline__ Hash128 mm_final(uint64_t h1, uint64_t h2, uint64_t len) {
+  h1 ^= len;
+  h2 ^= len;
+  h1 += h2;
+  h2 += h1;
+  h1 = fmix64(h1);
+  h2 = fmix64(h2);
+  h1 += h2;
+  h2 += h1;
+  return {h1, h2};
+}
+
+__device__ __forceinline__ uint64_t mm_k1(uint64_t k1) {
+  k1 *= MM_C1;
+  k1 = rotl64(k1, 31);
+  k1 *= MM_C2;
+  return k1;
+}
+__device__ __forceinline__ uint64_t mm_k2(uint64_t k2) {
+  k2 *= MM_C2;
+  k2 = rotl64(k2, 33);
+  k2 *= MM_C1;
+  return k2;
+}
+
+// Fast path: a u64 key == its 8-byte little-endian string. nblocks = 0,
+// tail k1 = the word, k2 = 0 (_kernels.py:118-136). Mixing a zero k1 is a
+// no-op, so the `if k1 != 0` guard needs no branch.
+__device__ __forceinline__ Hash128 murmur3_u64(uint64_t key, uint64_t seed) {
+  uint64_t h1 = seed ^ mm_k1(key);
+  return mm_final(h1, seed, 8ull);
+}
+
+// Variable-length path over a byte buffer (_kernels.py:89-146).
+// Loads are byte-granular through 8-byte assembled reads; buf may be
+// arbitrarily aligned.
+__device__ __forceinline__ uint64_t load_le(const uint8_t* __restrict__ p, int nbytes) {
+  uint64_t v = 0;
+#pragma unroll 8
+  for (int b = 0; b < nbytes; ++b) v |= (uint64_t)__ldg(p + b) << (8 * b);
+  return v;
+}
+
+__device__ __forceinline__ uint64_t load8_le(const uint8_t* __restrict__ p) {
+  // assemble from the two aligned 8-byte words that cover p..p+7
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  uintptr_t base = a & ~uintptr_t(7);
+  int sh = int(a - base);
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(base);
+  uint64_t lo = __ldg(w);
+  if (sh == 0) return lo;
+  uint64_t hi = __ldg(w + 1);
+  return (lo >> (8 * sh)) | (hi << (64 - 8 * sh));
+}
+
+__device__ __forceinline__ Hash128 murmur3_bytes(const uint8_t* __restrict__ key, int64_t len,
+                                                 uint64_t seed) {
+  uint64_t h1 = seed, h2 = seed;
+  int64_t nblocks = len >> 4;
+  for (int64_t blk = 0; blk < nblocks; ++blk) {
+    uint64_t k1 = load8_le(key + blk * 16);
+    uint64_t k2 = load8_le(key + blk * 16 + 8);
+    h1 ^= mm_k1(k1);
+    h1 = rotl64(h1, 27);
+    h1 += h2;
+    h1 = h1 * 5 + 0x52DCE729ull;
+    h2 ^= mm_k2(k2);
+    h2 = rotl64(h2, 31);
+    h2 += h1;
+    h2 = h2 * 5 + 0x38495AB5ull;
+  }
+  const uint8_t* tail = key + nblocks * 16;
+  int rem = int(len - nblocks * 16);
+  uint64_t k1 = 0, k2 = 0;
+  if (rem > 8) {
+    k1 = load8_le(tail);
+    k2 = load_le(tail + 8, rem - 8);
+  } else if (rem > 0) {
+    k1 = rem == 8 ? load8_le(tail) : load_le(tail, rem);
+  }
+  h2 ^= mm_k2(k2);
+  h1 ^= mm_k1(k1);
+  return mm_final(h1, h2, (uint64_t)len);
+}
+
+// Bucket of a high word (_kernels.py:158-167, assignment.py:124-161).
+// x = (f64(mix64(hi ^ SALT)) + 1) * 2^-64; t = 2048 x; k = int(t);
+// gamma = e[2048] if k >= 2048 else e[k] + (t - k) * (e[k+1] - e[k]);
+// b = clamp(ceil(gamma * B), 1, B). Each operation rounds on its own:
+// the explicit _rn intrinsics forbid FMA contraction.
+__device__ __forceinline__ uint32_t bucket_of(const double* __restrict__ e, uint64_t hi,
+                                              uint32_t bcount) {
+  uint64_t xb = mix64(hi ^ BUCKET_SALT);
+  double x = __dmul_rn(__dadd_rn(__ull2double_rn(xb), 1.0), 0x1p-64);
+  double t = __dmul_rn(x, 2048.0);
+  int k = __double2int_rz(t);
+  double g;
+  if (k >= GRID) {
+    g = __ldg(e + GRID);
+  } else {
+    double ek = __ldg(e + k), ek1 = __ldg(e + k + 1);
+    g = __dadd_rn(ek, __dmul_rn(__dsub_rn(t, (double)k), __dsub_rn(ek1, ek)));
+  }
+  double y = __dmul_rn(g, (double)bcount);
+  double c = ceil(y);
+  if (c < 1.0) return 1u;
+  if (c > (double)bcount) return bcount;
+  return (uint32_t)c;
+}
+
+__device__ __forceinline__ uint32_t position(uint64_t lo, uint64_t g, uint32_t m) {
+  return (uint32_t)mulhi(mix64(lo ^ g), (uint64_t)m);
+}
+
+// expected offset: round-half-up of j*n/nparts (partitioning.py:68-70)
+__host__ __device__ __forceinline__ int64_t expected_offset(int64_t j, int64_t n, int64_t nparts) {
+  unsigned __int128 num = (unsigned __int128)(2 * (uint64_t)j) * (uint64_t)n + (uint64_t)nparts;
+  return (int64_t)(num / (unsigned __int128)(2 * (uint64_t)nparts));
+}
+
+}  // namespace phb
+
+#define PHB_CUDA_TRY(expr)                   \
+  do {                                       \
+    cudaError_t _e = (expr);                 \
+    if (_e != cudaSuccess) return (int)_e;   \
+  } while (0)
