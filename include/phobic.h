@@ -73,6 +73,12 @@ int phb_query_many(const uint64_t* his, const uint64_t* los, int64_t nq, int64_t
                    int64_t nparts, const int64_t* deltas, const double* entries, int32_t bcount,
                    const uint64_t* seed_mat, int64_t* out, void* stream);
 
+/* Bucket ids of master-hash high words: clamp(ceil(gamma(x) * B), 1, B) with
+ * x = (f64(mix64(hi ^ SALT)) + 1) 2^-64 (_kernels._bucket_of, _kernels.py:158-167;
+ * assignment.bucket_many, assignment.py:146-149). out: u16[n]. */
+int phb_bucket_ids(const uint64_t* his, int64_t n, const double* entries, int32_t bcount,
+                   uint16_t* out, void* stream);
+
 /* ---------------------------------------------------------------------
  * Staged build pipeline (what pilothash.mphf.build, mphf.py:236-290,
  * becomes on B200). keys64 != NULL selects the u64 path, otherwise
@@ -156,6 +162,12 @@ int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint
  * (partitioning.offset, partitioning.py:119-122). */
 int phb_offsets_from_deltas(const int64_t* deltas, int64_t n, int64_t nparts, int64_t* key_off,
                             void* stream);
+
+/* Synthetic distinct 64-bit keys for benchmarks: out[i] = mix64(offset + i)
+ * (mix64 is a bijection on u64, so keys are distinct for distinct i). The
+ * host restatement is keygen.synth_u64. Not a reference interface: bench
+ * input generation. */
+int phb_synth_keys(uint64_t* out, int64_t n, uint64_t offset, void* stream);
 
 #ifdef __cplusplus
 }

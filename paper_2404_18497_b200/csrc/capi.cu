@@ -47,6 +47,12 @@ __global__ void k_offsets_from_deltas(const int64_t* __restrict__ deltas, int64_
     key_off[j] = expected_offset(j, n, nparts) + deltas[j];
 }
 
+__global__ void k_synth(uint64_t* __restrict__ out, int64_t n, uint64_t offset) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = mix64(offset + (uint64_t)i);
+}
+
 }  // namespace phb
 
 using namespace phb;
@@ -85,6 +91,13 @@ int phb_murmur3_u64(const uint64_t* keys, int64_t n, uint64_t seed, uint64_t* ou
                     uint64_t* out_lo, void* stream) {
   if (n < 0 || (n > 0 && !keys)) return PHB_E_ARGS;
   return launch_murmur(nullptr, nullptr, keys, n, seed, out_hi, out_lo, S(stream));
+}
+
+int phb_bucket_ids(const uint64_t* his, int64_t n, const double* entries, int32_t bcount,
+                   uint16_t* out, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (n < 0) return PHB_E_ARGS;
+  return launch_bucket_ids(his, n, entries, (uint32_t)bcount, out, S(stream));
 }
 
 int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
@@ -290,6 +303,14 @@ int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64
 int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad_flag,
                void* stream) {
   return launch_verify(out, nq, n, bitmap, bad_flag, S(stream));
+}
+
+int phb_synth_keys(uint64_t* out, int64_t n, uint64_t offset, void* stream) {
+  if (n < 0) return PHB_E_ARGS;
+  if (n == 0) return 0;
+  int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
+  k_synth<<<g, 256, 0, S(stream)>>>(out, n, offset);
+  return (int)cudaGetLastError();
 }
 
 }  // extern "C"

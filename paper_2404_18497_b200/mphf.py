@@ -1,0 +1,381 @@
+"""The queryable minimal perfect hash function and its device build.
+
+Mirrors pilothash.mphf (mphf.py:1-306): ``build(keys, config) -> Mphf``
+with the reference's retry policy (global_seed + attempt, 4 attempts, then
+``DuplicateKeys``, mphf.py:236-290), ``Mphf.query / query_many /
+is_bijection_on / bits_per_key / serialize / save / deserialize / load`` and
+the versioned little-endian format with a blake2b-8 checksum
+(mphf.py:156-233).
+
+The construction path is the device pipeline of ``BuildEngine``:
+  K1 phb_hash_count   murmur3 + partition index + per-partition counts
+  K2 phb_layout       key offsets, offset deltas, max |delta|, max size
+  K3 phb_scatter      re-hash, bucket id, scatter (lo, bucket) by partition
+  K4 phb_search       per-partition bucket order + bit-parallel seed search
+  K5 phb_encode_*     interleaved / mono Compact-Rice seeds + packed deltas
+                      assembled as the serialized body (from byte 57)
+Host work per attempt: two small synchronisations (max partition size for
+the search's shared-memory plan, and the status/size summary), the 57-byte
+fixed header and, for ``serialize``, blake2b over the body.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import struct
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native
+from .assignment import KIND_CODES, KINDS, AssignmentSpec, AssignmentTable, tabulate
+from .builder import BuildConfig, InvalidConfig, SeedExhausted, device_table
+from .encoders import MonoSeeds, SeedStore, parse_section
+from .keygen import DeviceKeys, as_corpus, to_device
+from .partitioning import PartitionLayout, num_partitions_for, unpack_deltas
+
+MAGIC = b"PHOB"
+VERSION = 1
+HEADER_BYTES = 16  # magic + version + n; excluded from bits/key (mphf.py:56)
+HEADER_FIXED = 57  # everything before the delta-width byte
+MAX_ATTEMPTS = 4   # mphf.py:58
+
+
+class DuplicateKeys(ValueError):
+    pass
+
+
+class FormatError(ValueError):
+    pass
+
+
+@dataclass
+class BuildStats:
+    attempts: int
+    trials_total: int
+    trials_per_key: float
+    build_seconds: float
+
+
+def _checksum(payload) -> int:
+    return int.from_bytes(hashlib.blake2b(payload, digest_size=8).digest(), "little")
+
+
+def _header(n: int, nparts: int, lambda_: float, psize: float, spec: AssignmentSpec,
+            global_seed: int) -> bytes:
+    return (MAGIC + struct.pack("<IQQdd", VERSION, n, nparts, lambda_, psize)
+            + struct.pack("<Bd", KIND_CODES[spec.kind], spec.epsilon)
+            + struct.pack("<Q", global_seed & 0xFFFFFFFFFFFFFFFF))
+
+
+@dataclass
+class DeviceBuild:
+    """Device-resident result of one successful pipeline pass."""
+
+    n: int
+    nparts: int
+    bcount: int
+    global_seed: int
+    key_off: torch.Tensor   # int64 [nparts + 1]
+    deltas: torch.Tensor    # int64 [nparts + 1]
+    seeds: torch.Tensor     # int64 view of u64, column-major [B][nparts]
+    blob: torch.Tensor      # uint8, serialized body (bytes [57, total) valid)
+    total_bytes: int
+    seed_section: int
+    trials_total: int
+
+
+class BuildEngine:
+    """One device build pass at a time; buffers come from torch's caching allocator."""
+
+    def __init__(self, config: BuildConfig, device: torch.device | None = None):
+        self.config = config
+        self.device = device or _native.require_device()
+        self.spec = config.resolved_assignment()
+        self.table: AssignmentTable = tabulate(self.spec)
+        self.entries = device_table(self.table, self.device)
+        self.bcount = config.bucket_count
+        self.mono, self.prefix = config.compact_prefix()
+        self._pinned = torch.zeros(2, dtype=torch.int64).pin_memory()
+        self._summary = np.zeros(8, np.int64)
+        self.last_launches = 0
+
+    def run(self, dk: DeviceKeys, seed: int) -> DeviceBuild | tuple[int, int]:
+        """One attempt. Returns DeviceBuild, or (first_bad, code) on failure."""
+        cfg, dev, B = self.config, self.device, self.bcount
+        n = dk.n
+        nparts = num_partitions_for(n, cfg.partition_size)
+        st = _native.stream()
+        P = _native.ptr
+        L = _native.lib()
+        seed &= 0xFFFFFFFFFFFFFFFF
+        k64 = P(dk.keys64) if dk.is_u64 else None
+        buf = None if dk.is_u64 else P(dk.buf)
+        offs = None if dk.is_u64 else P(dk.offsets)
+        launches = 0
+
+        counts = torch.zeros(nparts, dtype=torch.int32, device=dev)
+        _native.check(L.phb_hash_count(buf, offs, k64, n, seed, nparts, P(counts), st),
+                      "phb_hash_count")
+        key_off = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+        deltas = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+        stats = torch.empty(2, dtype=torch.int64, device=dev)
+        _native.check(L.phb_layout(P(counts), nparts, 0, 0, n, nparts, P(key_off), P(deltas),
+                                   P(stats), st), "phb_layout")
+        self._pinned.copy_(stats, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        counts.zero_()  # reused as the scatter cursors
+        lo = torch.empty(n, dtype=torch.int64, device=dev)
+        bid = torch.empty(n, dtype=torch.int16, device=dev)
+        _native.check(L.phb_scatter(buf, offs, k64, n, seed, nparts, P(self.entries), B,
+                                    P(key_off), P(counts), P(lo), P(bid), st), "phb_scatter")
+        seeds = torch.zeros(B * nparts, dtype=torch.int64, device=dev)
+        part_trials = torch.empty(nparts, dtype=torch.int64, device=dev)
+        status = torch.empty(nparts, dtype=torch.uint8, device=dev)
+        glo = torch.empty(n, dtype=torch.int64, device=dev)
+        queue = torch.empty(1, dtype=torch.int32, device=dev)
+        ev.synchronize()
+        m_max = int(self._pinned[1])
+        _native.check(L.phb_search(P(lo), P(bid), P(key_off), 0, nparts, 0, B, cfg.seed_cap,
+                                   cfg.tie_desc, m_max, P(seeds), 1, nparts, None,
+                                   P(part_trials), P(status), P(glo), P(queue), st),
+                      "phb_search")
+        ws = torch.empty(int(L.phb_encode_workspace_bytes(nparts, B, self.mono)),
+                         dtype=torch.uint8, device=dev)
+        summ = self._summary
+        _native.check(L.phb_encode_plan(P(seeds), nparts, B, self.mono, self.prefix, P(deltas),
+                                        nparts, P(stats), P(status), P(part_trials), P(ws),
+                                        summ.ctypes.data_as(ctypes.c_void_p), st),
+                      "phb_encode_plan")
+        if summ[3] >= 0:
+            return int(summ[3]), int(summ[4])
+        total = int(summ[0])
+        blob = torch.empty((total + 16 + 3) // 4 * 4, dtype=torch.uint8, device=dev)
+        _native.check(L.phb_encode_write(P(seeds), nparts, B, self.mono, self.prefix, P(deltas),
+                                         nparts, P(stats), P(ws), P(blob), blob.numel(), st),
+                      "phb_encode_write")
+        return DeviceBuild(n, nparts, B, seed, key_off, deltas, seeds, blob, total,
+                           int(summ[1]), int(summ[2]))
+
+
+class Mphf:
+    def __init__(self, global_seed: int, layout: PartitionLayout, table: AssignmentTable,
+                 bcount: int, seeds: SeedStore, lambda_: float, partition_size: float,
+                 stats: BuildStats | None = None):
+        self.global_seed = global_seed
+        self.layout = layout
+        self.table = table
+        self.bcount = bcount
+        self.seeds = seeds
+        self.lambda_ = lambda_
+        self.partition_size = partition_size
+        self.stats = stats
+        self._body: bytes | None = None  # serialized body without checksum
+        self._dev_key_off: torch.Tensor | None = None
+        self._dev_entries: torch.Tensor | None = None
+
+    # ---- construction from a device build -------------------------------
+    @classmethod
+    def _from_device(cls, db: DeviceBuild, config: BuildConfig, engine: BuildEngine,
+                     stats: BuildStats) -> "Mphf":
+        body = bytearray(db.blob[: db.total_bytes].cpu().numpy().tobytes())
+        head = _header(db.n, db.nparts, config.lambda_, config.partition_size, engine.spec,
+                       db.global_seed)
+        body[:HEADER_FIXED] = head
+        body = bytes(body)
+        deltas = db.deltas.cpu().numpy()
+        deltas.setflags(write=False)
+        layout = PartitionLayout(db.n, db.nparts, deltas)
+        store, _ = parse_section(body, db.seed_section, db.nparts, db.bcount)
+        store._device = db.seeds.view(db.bcount, db.nparts)
+        f = cls(db.global_seed, layout, engine.table, db.bcount, store, config.lambda_,
+                config.partition_size, stats)
+        f._body = body
+        f._dev_key_off = db.key_off
+        f._dev_entries = engine.entries
+        return f
+
+    # ---- properties -----------------------------------------------------
+    @property
+    def n(self) -> int:
+        return self.layout.n
+
+    @property
+    def encoder_name(self) -> str:
+        if isinstance(self.seeds, MonoSeeds):
+            return "mono-c" if self.seeds.compact_prefix else "mono-r"
+        t = self.seeds.compact_prefix
+        if t == 0:
+            return "ic-r"
+        if t >= self.bcount:
+            return "ic-c"
+        return f"mixed:{t}"
+
+    # ---- query ----------------------------------------------------------
+    def _device_state(self):
+        dev = _native.require_device()
+        if self._dev_key_off is None:
+            d = torch.from_numpy(np.ascontiguousarray(self.layout.deltas, np.int64)).to(dev)
+            key_off = torch.empty(self.layout.num_partitions + 1, dtype=torch.int64, device=dev)
+            _native.call("phb_offsets_from_deltas", _native.ptr(d), self.n,
+                         self.layout.num_partitions, _native.ptr(key_off), _native.stream())
+            self._dev_key_off = key_off
+        if self._dev_entries is None:
+            self._dev_entries = device_table(self.table, dev)
+        return self._dev_key_off, self._dev_entries, self.seeds.device_matrix()
+
+    def query_device(self, keys) -> torch.Tensor:
+        """Batched device query -> int64 CUDA tensor (query_many_kernel, _kernels.py:379-397)."""
+        dev = _native.require_device()
+        key_off, entries, seeds = self._device_state()
+        dk = keys if isinstance(keys, DeviceKeys) else to_device(keys, dev)
+        out = torch.empty(dk.n, dtype=torch.int64, device=dev)
+        P = _native.ptr
+        _native.call("phb_query", None if dk.is_u64 else P(dk.buf),
+                     None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
+                     dk.n, self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n,
+                     self.layout.num_partitions, P(key_off), P(entries), self.bcount, P(seeds),
+                     1, self.layout.num_partitions, P(out), _native.stream())
+        return out
+
+    def query_many(self, keys) -> np.ndarray:
+        return self.query_device(keys).cpu().numpy()
+
+    def query(self, key) -> int:
+        if isinstance(key, str):
+            key = key.encode("utf-8")
+        return int(self.query_many([bytes(key)])[0])
+
+    def verify_device(self, out: torch.Tensor) -> bool:
+        """Bijection of device outputs onto [0, n) (K8, replaces mphf.py:147-151)."""
+        if out.numel() != self.n:
+            return False
+        dev = out.device
+        bitmap = torch.zeros((self.n + 31) // 32, dtype=torch.int32, device=dev)
+        bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        _native.call("phb_verify", _native.ptr(out), out.numel(), self.n, _native.ptr(bitmap),
+                     _native.ptr(bad), _native.stream())
+        return int(bad.item()) == 0
+
+    def is_bijection_on(self, keys) -> bool:
+        return self.verify_device(self.query_device(keys))
+
+    # ---- format ---------------------------------------------------------
+    def _serialized_body(self) -> bytes:
+        if self._body is None:
+            from .partitioning import pack_deltas
+
+            width, packed = pack_deltas(self.layout.deltas)
+            spec = self.table.spec
+            self._body = (_header(self.n, self.layout.num_partitions, self.lambda_,
+                                  self.partition_size, spec, self.global_seed)
+                          + struct.pack("<B", width) + packed + struct.pack("<I", self.bcount)
+                          + self.seeds.section())
+        return self._body
+
+    def bits_per_key(self) -> float:
+        return (len(self._serialized_body()) + 8 - HEADER_BYTES) * 8 / self.n
+
+    def serialize(self) -> bytes:
+        body = self._serialized_body()
+        return body + struct.pack("<Q", _checksum(body))
+
+    def save(self, path) -> None:
+        with open(path, "wb") as f:
+            f.write(self.serialize())
+
+    @classmethod
+    def deserialize(cls, data: bytes) -> "Mphf":
+        """mphf.py:181-223: validate magic, version, checksum, then parse."""
+        data = bytes(data)
+        if len(data) < HEADER_BYTES + 8:
+            raise FormatError("input shorter than any valid structure")
+        if data[:4] != MAGIC:
+            raise FormatError("bad magic")
+        (version,) = struct.unpack_from("<I", data, 4)
+        if version != VERSION:
+            raise FormatError(f"unsupported version {version}")
+        (stored,) = struct.unpack_from("<Q", data, len(data) - 8)
+        if _checksum(data[:-8]) != stored:
+            raise FormatError("checksum mismatch")
+        try:
+            n, nparts, lambda_, psize, kind_code, epsilon, global_seed, width = struct.unpack_from(
+                "<QQddBdQB", data, 8)
+            at = HEADER_FIXED + 1
+            nbytes = ((nparts + 1) * width + 7) // 8
+            deltas = unpack_deltas(width, data[at: at + nbytes], nparts + 1)
+            at += nbytes
+            (bcount,) = struct.unpack_from("<I", data, at)
+            at += 4
+            if kind_code >= len(KINDS):
+                raise FormatError("unknown assignment kind")
+            store, at = parse_section(data, at, nparts, bcount)
+            if at != len(data) - 8:
+                raise FormatError("trailing bytes after seed section")
+        except (struct.error, ValueError, IndexError) as exc:
+            if isinstance(exc, FormatError):
+                raise
+            raise FormatError(f"malformed structure: {exc}") from exc
+        deltas.setflags(write=False)
+        layout = PartitionLayout(n=n, num_partitions=nparts, deltas=deltas)
+        table = tabulate(AssignmentSpec(KINDS[kind_code], epsilon))
+        f = cls(global_seed, layout, table, bcount, store, lambda_, psize)
+        f._body = data[:-8]
+        return f
+
+    @classmethod
+    def load(cls, path) -> "Mphf":
+        with open(path, "rb") as f:
+            return cls.deserialize(f.read())
+
+
+def build(keys, config: BuildConfig | None = None) -> Mphf:
+    """Construct an Mphf over distinct keys on the device (mphf.py:236-290).
+
+    keys: a KeyCorpus, an iterable of bytes/str, or a uint64 array / tensor
+    (host or CUDA; 64-bit keys hash as their 8-byte little-endian string).
+    """
+    config = config or BuildConfig()
+    dev = _native.require_device()
+    t0 = time.perf_counter()
+    dk = to_device(keys, dev)
+    if dk.n < 1:
+        raise InvalidConfig("need at least one key")
+    engine = BuildEngine(config, dev)
+    last: str | None = None
+    for attempt in range(MAX_ATTEMPTS):
+        seed = config.global_seed + attempt
+        res = engine.run(dk, seed)
+        if isinstance(res, tuple):
+            bad, code = res
+            reason = "unseparable duplicate hashes" if code == 1 else "seed cap hit"
+            last = f"partition {bad}: {reason}"
+            continue
+        stats = BuildStats(attempts=attempt + 1, trials_total=res.trials_total,
+                           trials_per_key=res.trials_total / dk.n, build_seconds=0.0)
+        f = Mphf._from_device(res, config, engine, stats)
+        stats.build_seconds = time.perf_counter() - t0
+        return f
+    raise DuplicateKeys(
+        f"construction failed after {MAX_ATTEMPTS} seeds ({SeedExhausted(last)}); "
+        "input most likely contains duplicate keys")
+
+
+def query(f: Mphf, key) -> int:
+    return f.query(key)
+
+
+def serialize(f: Mphf) -> bytes:
+    return f.serialize()
+
+
+def deserialize(data: bytes) -> Mphf:
+    return Mphf.deserialize(data)
+
+
+def bits_per_key(f: Mphf) -> float:
+    return f.bits_per_key()
