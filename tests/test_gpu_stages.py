@@ -148,7 +148,8 @@ def _device_search(nat, orc, m, hs, ls, key_off, tie_desc, shuffle=False):
     status = torch.zeros(nparts, dtype=torch.uint8, device=DEV)
     tab = torch.from_numpy(table).to(DEV)
     koff = torch.from_numpy(key_off).to(DEV)
-    nat.call("phb_build_partition_range", nat.ptr(u64t(hs)), nat.ptr(u64t(ls)), nat.ptr(koff), 0,
+    dhs, dls = u64t(hs), u64t(ls)  # keep alive across the call (caching allocator)
+    nat.call("phb_build_partition_range", nat.ptr(dhs), nat.ptr(dls), nat.ptr(koff), 0,
              nparts, nat.ptr(tab), B, m.get("seed_cap", 1 << 40), int(tie_desc), nat.ptr(seeds),
              nat.ptr(trials), nat.ptr(status), nat.stream())
     return (host_u64(seeds).reshape(nparts, B), trials.cpu().numpy().reshape(nparts, B),
