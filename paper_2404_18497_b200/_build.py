@@ -17,7 +17,7 @@ OBJ = PKG / "_obj"
 LIB = PKG / "libphobic_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
+FLAGS = os.environ.get("PHB_NVCC_EXTRA", "").split() + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
          "--expt-relaxed-constexpr"]
 SOURCES = ["hash.cu", "layout.cu", "search.cu", "encode.cu", "decode.cu", "query.cu", "capi.cu"]
 

@@ -11,43 +11,49 @@
 // Design (B200):
 //  * One warp owns one partition; partitions come from a global atomic
 //    work queue, so heavy-tailed partitions (bucket 1 birthday searches,
-//    SURVEY.md §0 finding 7) load-balance dynamically across ~40 resident
-//    warps per SM. No __syncthreads anywhere: warps are independent.
+//    SURVEY.md §0 finding 7) load-balance dynamically across the resident
+//    warps. No __syncthreads anywhere: warps are independent.
 //  * Per-warp shared memory holds only bitmaps and bucket metadata
-//    (~4-6 KB): a doubled occupancy bitmap (2m bits, so a cyclic window is
-//    one funnel shift), an m-bit self-collision scratch map, bucket sizes /
-//    offsets and the processing order. Keys stay in L1/L2 (bucket-grouped
-//    scratch `glo`) and in registers (<= 256 keys per bucket).
+//    (~5 KB at lambda = 9): a doubled occupancy bitmap (2m bits, so a cyclic
+//    window is one funnel shift), an m-bit self-collision scratch map,
+//    bucket sizes / offsets, the processing order and the current bucket's
+//    base positions. Keys stay in L1/L2 (bucket-grouped scratch `glo`).
 //  * Displacement search is bit-parallel: valid(d) = AND_i free(p_i + d).
-//    Lane l evaluates d in [1024c + 32l, +32) as one u32 word; a ballot +
-//    ffs picks the smallest d. 32 lanes x 32 bits = 1024 displacements per
-//    step, with an early exit once every lane's word is saturated.
+//    Lane l owns the three consecutive 32-bit words [3l, 3l+3) of the valid
+//    mask (96 words = 3072 displacements per pass, conflict-free since 3 is
+//    odd), i.e. 4 shared loads + 3 funnel shifts per key; a ballot + ffs
+//    picks the smallest d. Every 4 keys the warp stops early once all
+//    words are saturated.
 //  * Self-collision of a candidate s: __match_any_sync on positions for
 //    k <= 32, shared-memory atomicOr test-and-set for larger buckets.
 //  * Trials use the closed form k * (S_self + sum_fail(dmax+1) + d* + 1),
 //    identical to the reference's per-candidate counting.
+#include <cstdio>
 #include "common.cuh"
 #include "phobic_internal.h"
 
 namespace phb {
 
-constexpr int KREG = 8;    // key rounds held in registers: buckets up to 256 keys
-constexpr int SH = 256;    // size classes of the counting-sort bucket order
-constexpr int WARPS = 4;   // warps (= partitions in flight) per CTA
+constexpr int SH = 256;     // size classes of the counting-sort bucket order
+constexpr int PMAX = 256;   // bucket sizes whose base positions are staged in smem
+constexpr int WARPS = 4;    // warps (= partitions in flight) per CTA
 constexpr unsigned FULL = 0xffffffffu;
 
+// Per-warp shared-memory plan, in 32-bit words.
 struct SmemPlan {
-  int occ_w, scr_w, cnt_w, ord_w, sh_w, total_w;
+  int occ_w, scr_w, cnt_w, ord_w, sh_w, pos_w, total_w;
 };
 
 __host__ __device__ inline SmemPlan smem_plan(int64_t m_max, uint32_t bcount) {
   SmemPlan p;
-  p.occ_w = (int)((2 * m_max + 64) / 32 + 2);
+  // reads reach word (m-1)/32 + 3*31 + 3 of a pass, marks reach bit 2m - 1
+  p.occ_w = (int)((2 * m_max) / 32 + 104);
   p.scr_w = (int)(m_max / 32 + 2);
   p.cnt_w = (int)bcount + 1;  // cnt and endp each
   p.ord_w = (int)(bcount + 2) / 2;
-  p.sh_w = SH;  // shist + srun as u16
-  p.total_w = p.occ_w + p.scr_w + 2 * p.cnt_w + p.ord_w + p.sh_w;
+  p.sh_w = SH;       // shist + srun as u16
+  p.pos_w = PMAX / 2;  // u16 base positions
+  p.total_w = p.occ_w + p.scr_w + 2 * p.cnt_w + p.ord_w + p.sh_w + p.pos_w;
   p.total_w += p.total_w & 1;
   return p;
 }
@@ -73,28 +79,29 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return r;
 }
 
-__device__ __forceinline__ uint32_t window(const uint32_t* occ, uint32_t q) {
-  uint32_t w = q >> 5;
-  return __funnelshift_r(occ[w], occ[w + 1], q & 31);
-}
+extern __shared__ uint32_t smem[];
 
-__device__ __forceinline__ void mark(uint32_t* occ, uint32_t slot, uint32_t m) {
-  atomicOr(occ + (slot >> 5), 1u << (slot & 31));
-  uint32_t s2 = slot + m;
-  atomicOr(occ + (s2 >> 5), 1u << (s2 & 31));
+__device__ __forceinline__ void mark(uint32_t occ, uint32_t slot, uint32_t m, int tag = 0) {
+#ifdef PHB_DEBUG
+  if (slot >= m) { printf("mark: slot %u m %u tag %d\n", slot, m, tag); __trap(); }
+  if (smem[occ + (slot >> 5)] & (1u << (slot & 31))) { printf("mark: slot %u already taken (m %u) tag %d\n", slot, m, tag); __trap(); }
+#endif
+  atomicOr(&smem[occ + (slot >> 5)], 1u << (slot & 31));
+  const uint32_t s2 = slot + m;
+  atomicOr(&smem[occ + (s2 >> 5)], 1u << (s2 & 31));
 }
 
 // Processing order of the non-empty buckets (_kernels.py:268-282):
 // size descending, ties by `tie` descending where tie = b ("asc-expected",
 // tie_desc = 1) or B - b. Returns the number of non-empty buckets.
-__device__ uint32_t bucket_order(const uint32_t* cnt, uint32_t B, int tie_desc, uint32_t maxsz,
+__device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_t maxsz,
                                  uint16_t* order, uint16_t* shist, uint16_t* srun, int lane) {
   if (maxsz < (uint32_t)SH) {
     for (int s = lane; s < SH; s += 32) shist[s] = 0, srun[s] = 0;
     __syncwarp();
     for (uint32_t c0 = 1; c0 <= B; c0 += 32) {
       uint32_t b = c0 + lane;
-      uint32_t sz = b <= B ? cnt[b] : 0u;
+      uint32_t sz = b <= B ? smem[cnt + b] : 0u;
       uint32_t peers = __match_any_sync(FULL, sz);
       if (sz > 0 && lane == __ffs(peers) - 1) shist[sz] += (uint16_t)__popc(peers);
       __syncwarp();
@@ -113,7 +120,7 @@ __device__ uint32_t bucket_order(const uint32_t* cnt, uint32_t B, int tie_desc, 
     for (uint32_t c0 = 0; c0 < B; c0 += 32) {
       uint32_t idx = c0 + lane;
       uint32_t b = tie_desc ? (B - idx) : (idx + 1);
-      uint32_t sz = idx < B ? cnt[b] : 0u;
+      uint32_t sz = idx < B ? smem[cnt + b] : 0u;
       uint32_t peers = __match_any_sync(FULL, sz);
       if (sz > 0) order[shist[sz] + srun[sz] + __popc(peers & lanemask_lt())] = (uint16_t)b;
       __syncwarp();
@@ -126,12 +133,12 @@ __device__ uint32_t bucket_order(const uint32_t* cnt, uint32_t B, int tie_desc, 
   uint32_t nb = 0;
   for (uint32_t c0 = 1; c0 <= B; c0 += 32) {
     uint32_t b = c0 + lane;
-    uint32_t sz = b <= B ? cnt[b] : 0u;
+    uint32_t sz = b <= B ? smem[cnt + b] : 0u;
     if (sz > 0) {
       uint64_t key = (uint64_t)sz * (B + 1) + (tie_desc ? b : B - b);
       uint32_t rank = 0;
       for (uint32_t b2 = 1; b2 <= B; ++b2) {
-        uint32_t s2 = cnt[b2];
+        uint32_t s2 = smem[cnt + b2];
         uint64_t k2 = (uint64_t)s2 * (B + 1) + (tie_desc ? b2 : B - b2);
         rank += (s2 > 0 && k2 > key);
       }
@@ -144,71 +151,278 @@ __device__ uint32_t bucket_order(const uint32_t* cnt, uint32_t B, int tie_desc, 
 }
 
 // First displacement d in [0, dmax] with every key's slot free, or -1.
-// pos[r] holds the base positions of key 32r + lane (registers, r < KREG);
-// rounds beyond KREG re-derive positions from the key scratch.
-__device__ __forceinline__ int64_t first_valid(const uint32_t* occ, const uint32_t (&pos)[KREG],
-                                               uint32_t k, int64_t dmax, const uint64_t* kl,
-                                               uint64_t g, uint32_t m, int lane) {
-  const uint32_t R = (k + 31) >> 5;
-  const uint32_t nch = (uint32_t)((dmax + 1024) >> 10);
-  for (uint32_t c = 0; c < nch; ++c) {
-    const int64_t dbase = (int64_t)c * 1024 + lane * 32;
-    const bool live = dbase <= dmax;
-    const uint32_t db = (uint32_t)dbase;
-    uint32_t acc = live ? 0u : FULL;
-    bool dead = false;
-#pragma unroll
-    for (int r = 0; r < KREG; ++r) {
-      if ((uint32_t)r < R && !dead) {
-        const uint32_t kr = min(32u, k - 32u * r);
-        for (uint32_t src = 0; src < kr; ++src) {
-          uint32_t p = __shfl_sync(FULL, pos[r], src);
-          if (live) acc |= window(occ, p + db);
-          if ((src & 7) == 7 && __all_sync(FULL, acc == FULL)) {
-            dead = true;
-            break;
-          }
-        }
-      }
+// Base positions come from the staged u16 list (k <= PMAX) or are re-derived
+// from the key scratch (larger buckets).
+__device__ __forceinline__ int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t k,
+                                          int64_t dmax, const uint64_t* kl, uint64_t g,
+                                          uint32_t m, int lane) {
+  const uint32_t nwd = (uint32_t)((dmax + 32) >> 5);  // words of the valid mask
+  for (uint32_t g0 = 0; g0 < nwd; g0 += 96) {
+    const uint32_t wb = g0 + 3u * lane;
+    uint32_t a0 = 0, a1 = 0, a2 = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint32_t p = k <= (uint32_t)PMAX ? (uint32_t)pos16[i] : position(kl[i], g, m);
+      const uint32_t W = occ + (p >> 5) + wb;
+      const uint32_t sh = p & 31;
+      const uint32_t x0 = smem[W], x1 = smem[W + 1], x2 = smem[W + 2], x3 = smem[W + 3];
+      a0 |= __funnelshift_r(x0, x1, sh);
+      a1 |= __funnelshift_r(x1, x2, sh);
+      a2 |= __funnelshift_r(x2, x3, sh);
+      if ((i & 3) == 3 && __all_sync(FULL, (a0 & a1 & a2) == FULL)) break;
     }
-    for (uint32_t r = KREG; r < R && !dead; ++r) {
-      const uint32_t kr = min(32u, k - 32u * r);
-      uint32_t mine = lane < kr ? position(kl[32 * r + lane], g, m) : 0u;
-      for (uint32_t src = 0; src < kr; ++src) {
-        uint32_t p = __shfl_sync(FULL, mine, src);
-        if (live) acc |= window(occ, p + db);
-        if ((src & 7) == 7 && __all_sync(FULL, acc == FULL)) {
-          dead = true;
-          break;
-        }
-      }
+    // restrict to d <= dmax; lanes past the end contribute nothing
+    uint32_t v0 = ~a0, v1 = ~a1, v2 = ~a2;
+    const int64_t lim = dmax - 32 * (int64_t)wb;  // last valid bit index in word wb
+    if (lim < 95) {
+      v0 = lim < 0 ? 0u : (lim < 31 ? v0 & ((2u << lim) - 1u) : v0);
+      v1 = lim < 32 ? 0u : (lim < 63 ? v1 & ((2u << (lim - 32)) - 1u) : v1);
+      v2 = lim < 64 ? 0u : (lim < 95 ? v2 & ((2u << (lim - 64)) - 1u) : v2);
     }
-    uint32_t valid = ~acc;
-    if (live) {
-      int64_t rem = dmax - dbase;
-      if (rem < 31) valid &= (2u << rem) - 1u;
-    }
-    uint32_t bal = __ballot_sync(FULL, valid != 0);
+    const uint32_t bal = __ballot_sync(FULL, (v0 | v1 | v2) != 0);
     if (bal) {
-      int l = __ffs(bal) - 1;
-      uint32_t vv = __shfl_sync(FULL, valid, l);
-      return (int64_t)c * 1024 + l * 32 + (__ffs(vv) - 1);
+      const int l = __ffs(bal) - 1;
+      const uint32_t t = v0 ? 0u : (v1 ? 1u : 2u);
+      const uint32_t vv = v0 ? v0 : (v1 ? v1 : v2);
+      const uint32_t word = __shfl_sync(FULL, t, l);
+      const uint32_t bits = __shfl_sync(FULL, vv, l);
+      return 32 * (int64_t)(g0 + 3u * l + word) + (__ffs(bits) - 1);
     }
   }
   return -1;
 }
 
-__global__ void __launch_bounds__(WARPS * 32) k_search(SearchArgs a, SmemPlan plan) {
-  extern __shared__ uint32_t smem[];
+
+// Outcome of one bucket's search.
+struct BucketResult {
+  int64_t seed, trials;
+  int status;  // 0 found, 1 duplicate low words, 2 seed cap
+};
+
+// Generic single-s search (any k, any m): the reference loop of
+// _kernels.py:312-369 with each s tested by the whole warp.
+__device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos16, uint32_t k,
+                                       const uint64_t* kl, uint32_t m, int64_t cap,
+                                       int64_t s_begin, int64_t trials, int lane) {
+  const uint32_t R = (k + 31) >> 5;
+  const uint32_t amask = k >= 32 ? FULL : ((1u << k) - 1u);
+  const uint64_t key0 = (uint32_t)lane < k ? kl[lane] : 0ull;
+  const uint32_t scr_used = m / 32 + 2;
+  uint32_t p0 = 0;  // this lane's base position (k <= 32)
+  for (int64_t s = s_begin;; ++s) {
+    const int64_t pbase = s * (int64_t)m;
+    if (s > 0 && pbase > cap) return {0, trials, 2};  // _kernels.py:324-328
+    const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
+    bool coll = false;
+    uint32_t cmask = 0;  // per-round collision flags (s = 0 duplicate check)
+    if (k <= 32) {
+      p0 = position(key0, g, m);
+      const uint32_t peers = __match_any_sync(FULL, p0) & amask;
+      coll = __any_sync(FULL, (uint32_t)lane < k && __popc(peers) > 1);
+      if (!coll && (uint32_t)lane < k) pos16[lane] = (uint16_t)p0;
+    } else {
+      for (uint32_t r = 0; r < R; ++r) {
+        const uint32_t i = 32u * r + lane;
+        bool c = false;
+        if (i < k) {
+          const uint32_t p = position(kl[i], g, m);
+          const uint32_t bit = 1u << (p & 31);
+          c = (atomicOr(&smem[scr + (p >> 5)], bit) & bit) != 0;
+          if (i < (uint32_t)PMAX) pos16[i] = (uint16_t)p;
+        }
+        if (r < 32) cmask |= (uint32_t)c << r;
+        if (__any_sync(FULL, c)) {
+          coll = true;
+          if (s > 0) break;  // s = 0 inserts every key for the dup check
+        }
+      }
+      __syncwarp();
+      for (uint32_t w = lane; w < scr_used; w += 32) smem[scr + w] = 0;
+    }
+    __syncwarp();
+    if (s == 0) {
+      // duplicate low words collide at every s, so they can only exist if
+      // s = 0 collides (_kernels.py:312-319)
+      if (coll) {
+        bool dup = false;
+        if (k <= 32) {
+          const uint32_t peers = __match_any_sync(FULL, key0) & amask;
+          dup = (uint32_t)lane < k && __popc(peers) > 1;
+        } else if (R <= 32) {
+          // a duplicate pair's later key found its slot taken: compare every
+          // key that collided against the whole bucket
+          for (uint32_t r = 0; r < R; ++r) {
+            uint32_t bal = __ballot_sync(FULL, (cmask >> r) & 1u);
+            while (bal) {
+              const uint32_t src = 32u * r + (__ffs(bal) - 1);
+              bal &= bal - 1;
+              const uint64_t v = kl[src];
+              for (uint32_t i2 = lane; i2 < k; i2 += 32)
+                if (i2 != src && kl[i2] == v) dup = true;
+            }
+          }
+        } else {
+          for (uint32_t i = 0; i < k; ++i) {
+            const uint64_t v = kl[i];
+            for (uint32_t i2 = lane; i2 < k; i2 += 32)
+              if (i2 != i && kl[i2] == v) dup = true;
+          }
+        }
+        if (__any_sync(FULL, dup)) return {0, trials, 1};
+      }
+      if (pbase > cap) return {0, trials, 2};
+    }
+    if (coll) {
+      trials += k;
+      continue;
+    }
+    int64_t dmax = cap - pbase;
+    if (dmax > (int64_t)m - 1) dmax = (int64_t)m - 1;
+    const int64_t d = find_d(occ, pos16, k, dmax, kl, g, m, lane);
+    if (d >= 0) {
+      trials += (int64_t)k * (d + 1);
+      for (uint32_t i = lane; i < k; i += 32) {
+        const uint32_t p =
+            k <= 32 ? p0 : (i < (uint32_t)PMAX ? (uint32_t)pos16[i] : position(kl[i], g, m));
+        uint32_t slot = p + (uint32_t)d;
+        if (slot >= m) slot -= m;
+        mark(occ, slot, m, 2000 + (int)k);
+      }
+      return {pbase + d, trials, 0};
+    }
+    trials += (int64_t)k * (dmax + 1);
+  }
+}
+
+// Batched search for small buckets (k <= 32 / G) in partitions with
+// m <= 3072: G consecutive seeds s are tested per step, one group of
+// L = 32 / G lanes per seed, each lane owning WPL = 96 / L consecutive
+// words of that seed's valid mask (WPL + 1 shared loads per key). The
+// groups are then resolved in seed order exactly like the sequential
+// loop, so seeds and trials are unchanged. Returns status -1 when
+// max_batches ran out without a decision (the caller continues).
+template <int G>
+__device__ BucketResult small_bucket(uint32_t occ, uint16_t* pos16, uint32_t k,
+                                     const uint64_t* kl, uint32_t m, int64_t cap,
+                                     int64_t& s_next, int64_t trials, int max_batches,
+                                     int lane) {
+  constexpr int L = 32 / G, WPL = 96 / L;
+  const int grp = lane / L, gl = lane % L;
+  const bool act = (uint32_t)gl < k;
+  const uint64_t key = act ? kl[gl] : 0ull;
+  const uint32_t gmask = L == 32 ? FULL : (((1u << L) - 1u) << (grp * L));
+  uint16_t* const mypos = pos16 + grp * L;
+  for (int bt = 0; bt < max_batches; ++bt) {
+    const int64_t s = s_next + grp;
+    const int64_t pbase = s * (int64_t)m;
+    const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
+    const uint32_t p = position(key, g, m);
+    const uint32_t tag = act ? (((uint32_t)grp << 16) | p) : (0x80000000u | (uint32_t)lane);
+    // every lane must execute the vote (no short-circuit around it)
+    const uint32_t tpeers = __match_any_sync(FULL, tag);
+    const bool mycoll = act && __popc(tpeers) > 1;
+    const uint32_t cball = __ballot_sync(FULL, mycoll);
+#ifdef PHB_DEBUG
+    {
+      bool bf = false;
+      for (int o = 0; o < 32; ++o) {
+        uint32_t t2 = __shfl_sync(FULL, tag, o);
+        if (o != lane && t2 == tag && act) bf = true;
+      }
+      if (bf != mycoll) printf("match_any mismatch lane %d tag %x k %u G %d\n", lane, tag, k, G);
+    }
+#endif
+    if (act) mypos[gl] = (uint16_t)p;
+    __syncwarp();
+    const bool gcoll = (cball & gmask) != 0;
+    const bool gcap = pbase > cap;
+    int64_t dmax = cap - pbase;
+    if (dmax > (int64_t)m - 1) dmax = (int64_t)m - 1;
+    uint32_t acc[WPL];
+    const bool dead_group = gcoll || gcap;
+#pragma unroll
+    for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : 0u;
+    const uint32_t wb = (uint32_t)gl * WPL;
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint32_t pi = mypos[i];
+      const uint32_t W = occ + (pi >> 5) + wb;
+      const uint32_t sh = pi & 31;
+      uint32_t x = smem[W];
+#pragma unroll
+      for (int t = 0; t < WPL; ++t) {
+        const uint32_t y = smem[W + t + 1];
+        acc[t] |= __funnelshift_r(x, y, sh);
+        x = y;
+      }
+      if ((i & 3) == 3) {
+        uint32_t all = FULL;
+#pragma unroll
+        for (int t = 0; t < WPL; ++t) all &= acc[t];
+        if (__all_sync(FULL, all == FULL)) break;
+      }
+    }
+    // this lane's first valid displacement (d <= dmax), or -1
+    int64_t myd = -1;
+    const int64_t lim = dmax - 32 * (int64_t)wb;
+#pragma unroll
+    for (int t = WPL - 1; t >= 0; --t) {
+      uint32_t v = ~acc[t];
+      const int64_t lt = lim - 32 * t;
+      v = lt < 0 ? 0u : (lt < 31 ? v & ((2u << lt) - 1u) : v);
+      if (v) myd = 32 * (int64_t)(wb + t) + (__ffs(v) - 1);
+    }
+    const uint32_t fball = __ballot_sync(FULL, myd >= 0);
+    // resolve the G seeds in order, like the sequential loop
+    for (int gi = 0; gi < G; ++gi) {
+      const int64_t si = s_next + gi;
+      const int64_t pb = si * (int64_t)m;
+      const uint32_t gm = L == 32 ? FULL : (((1u << L) - 1u) << (gi * L));
+      const bool ci = (cball & gm) != 0;
+      if (si > 0 && pb > cap) return {0, trials, 2};
+      if (si == 0) {
+        if (ci) {
+          const uint32_t peers = __match_any_sync(FULL, key) & gm & __ballot_sync(FULL, act);
+          const bool dup = grp == gi && act && __popc(peers) > 1;
+          if (__any_sync(FULL, dup)) return {0, trials, 1};
+        }
+        if (pb > cap) return {0, trials, 2};
+      }
+      if (ci) {
+        trials += k;
+        continue;
+      }
+      int64_t dmi = cap - pb;
+      if (dmi > (int64_t)m - 1) dmi = (int64_t)m - 1;
+      const uint32_t fb = fball & gm;
+      if (fb) {
+        const int64_t d = __shfl_sync(FULL, myd, __ffs(fb) - 1);
+        trials += (int64_t)k * (d + 1);
+        if (grp == gi && act) {
+          uint32_t slot = p + (uint32_t)d;
+          if (slot >= m) slot -= m;
+          mark(occ, slot, m, 100 * G + (int)k);
+        }
+        return {pb + d, trials, 0};
+      }
+      trials += (int64_t)k * (dmi + 1);
+    }
+    s_next += G;
+    __syncwarp();
+  }
+  return {0, trials, -1};
+}
+
+__global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan plan) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t B = a.bcount;
-  uint32_t* occ = smem + wid * plan.total_w;
-  uint32_t* scr = occ + plan.occ_w;
-  uint32_t* cnt = scr + plan.scr_w;
-  uint32_t* endp = cnt + plan.cnt_w;
-  uint16_t* order = reinterpret_cast<uint16_t*>(endp + plan.cnt_w);
-  uint16_t* shist = order + 2 * plan.ord_w;
-  uint16_t* srun = shist + SH;
+  const uint32_t occ = wid * plan.total_w;
+  const uint32_t scr = occ + plan.occ_w;
+  const uint32_t cnt = scr + plan.scr_w;
+  const uint32_t endp = cnt + plan.cnt_w;
+  uint16_t* const sm16 = reinterpret_cast<uint16_t*>(smem);
+  uint16_t* const order = sm16 + 2 * (endp + plan.cnt_w);
+  uint16_t* const shist = order + 2 * plan.ord_w;
+  uint16_t* const srun = shist + SH;
+  uint16_t* const pos16 = srun + SH;
   const int64_t nrange = a.p_hi - a.p_lo;
   const uint64_t g0 = mix64(POSITION_SALT);  // s = 0
   const int64_t cap = a.seed_cap;
@@ -230,31 +444,31 @@ __global__ void __launch_bounds__(WARPS * 32) k_search(SearchArgs a, SmemPlan pl
       continue;
     }
 
-    // ---- bucket histogram + stable-free counting sort (_kernels.py:252-266)
-    for (uint32_t b = lane; b <= B; b += 32) cnt[b] = 0;
+    // ---- bucket histogram + counting sort into glo (_kernels.py:252-266)
+    for (uint32_t b = lane; b <= B; b += 32) smem[cnt + b] = 0;
     __syncwarp();
-    for (uint32_t q = lane; q < m; q += 32) atomicAdd(cnt + a.bid[kb + q], 1u);
+    for (uint32_t q = lane; q < m; q += 32) atomicAdd(&smem[cnt + a.bid[kb + q]], 1u);
     __syncwarp();
     uint32_t run = 0, maxsz = 0;
     for (uint32_t c0 = 1; c0 <= B; c0 += 32) {
       uint32_t b = c0 + lane;
-      uint32_t v = b <= B ? cnt[b] : 0u;
+      uint32_t v = b <= B ? smem[cnt + b] : 0u;
       uint32_t inc = warp_incl_scan(v, lane);
-      if (b <= B) endp[b] = run + inc - v;
+      if (b <= B) smem[endp + b] = run + inc - v;
       run += __shfl_sync(FULL, inc, 31);
       maxsz = max(maxsz, v);
     }
     maxsz = warp_max(maxsz);
     __syncwarp();
     for (uint32_t q = lane; q < m; q += 32) {
-      uint32_t b = a.bid[kb + q];
-      uint32_t at = atomicAdd(endp + b, 1u);
+      const uint32_t b = a.bid[kb + q];
+      const uint32_t at = atomicAdd(&smem[endp + b], 1u);
       a.glo[kb + at] = a.lo[kb + q];
     }
-    const uint32_t occ_used = (2 * m + 64) / 32 + 2;
-    for (uint32_t w = lane; w < occ_used; w += 32) occ[w] = 0;
+    const uint32_t occ_used = min((uint32_t)plan.occ_w, (2 * m) / 32 + 104);
+    for (uint32_t w = lane; w < occ_used; w += 32) smem[occ + w] = 0;
     const uint32_t scr_used = m / 32 + 2;
-    for (uint32_t w = lane; w < scr_used; w += 32) scr[w] = 0;
+    for (uint32_t w = lane; w < scr_used; w += 32) smem[scr + w] = 0;
     __syncwarp();
 
     const uint32_t nb = bucket_order(cnt, B, a.tie_desc, maxsz, order, shist, srun, lane);
@@ -263,154 +477,49 @@ __global__ void __launch_bounds__(WARPS * 32) k_search(SearchArgs a, SmemPlan pl
     // ---- seed search, bucket by bucket (_kernels.py:295-369)
     int64_t ptrials = 0;
     uint8_t status = 0;
+    const bool small_ok = m <= 3072;
     for (uint32_t oi = 0; oi < nb; ++oi) {
       const uint32_t b = order[oi];
-      const uint32_t k = cnt[b];
-      const uint64_t* kl = a.glo + kb + (endp[b] - k);
-      int64_t seed = 0, trials = 0;
+      const uint32_t k = smem[cnt + b];
+      const uint64_t* kl = a.glo + kb + (smem[endp + b] - k);
+      BucketResult res;
       if (k == 1) {
         // singleton: first free slot cyclically from the s = 0 base; no cap
-        // (_kernels.py:300-310). Same first_valid machinery with one key.
+        // (_kernels.py:300-310)
         const uint32_t p = position(kl[0], g0, m);
-        uint32_t pos[KREG] = {};
-        pos[0] = p;
-        int64_t d = first_valid(occ, pos, 1, (int64_t)m - 1, kl, g0, m, lane);
+        if (lane == 0) pos16[0] = (uint16_t)p;
+        __syncwarp();
+        const int64_t d = find_d(occ, pos16, 1, (int64_t)m - 1, kl, g0, m, lane);
         uint32_t slot = p + (uint32_t)d;
         if (slot >= m) slot -= m;
-        if (lane == 0) mark(occ, slot, m);
-        seed = d;
-        trials = d + 1;
+        if (lane == 0) mark(occ, slot, m, 1);
+        res = {d, d + 1, 0};
+      } else if (small_ok && k <= 32) {
+        // one single-seed step first (sparse tables usually succeed at s = 0),
+        // then batches of G seeds
+        int64_t s_next = 0;
+        res = small_bucket<1>(occ, pos16, k, kl, m, cap, s_next, 0, 1, lane);
+        if (res.status < 0) {
+          if (k <= 8)
+            res = small_bucket<4>(occ, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+          else if (k <= 16)
+            res = small_bucket<2>(occ, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+          else
+            res = small_bucket<1>(occ, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+        }
       } else {
-        const uint32_t R = (k + 31) >> 5;
-        const uint32_t amask = k >= 32 ? FULL : ((1u << k) - 1u);
-        uint64_t key[KREG];
-        uint32_t pos[KREG];
-#pragma unroll
-        for (int r = 0; r < KREG; ++r) {
-          uint32_t i = 32u * r + lane;
-          key[r] = ((uint32_t)r < R && i < k) ? kl[i] : 0ull;
-          pos[r] = 0;
-        }
-        for (int64_t s = 0;; ++s) {
-          const int64_t pbase = s * (int64_t)m;
-          if (s > 0 && pbase > cap) {  // _kernels.py:324-328
-            status = 2;
-            break;
-          }
-          const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
-          bool coll = false;
-          if (k <= 32) {
-            pos[0] = position(key[0], g, m);
-            uint32_t peers = __match_any_sync(FULL, pos[0]) & amask;
-            coll = __any_sync(FULL, lane < (int)k && __popc(peers) > 1);
-          } else {
-#pragma unroll
-            for (int r = 0; r < KREG; ++r) {
-              if ((uint32_t)r < R && !coll) {
-                uint32_t i = 32u * r + lane;
-                pos[r] = position(key[r], g, m);
-                bool c = false;
-                if (i < k) {
-                  uint32_t bit = 1u << (pos[r] & 31);
-                  c = (atomicOr(scr + (pos[r] >> 5), bit) & bit) != 0;
-                }
-                coll = __any_sync(FULL, c);
-              }
-            }
-            for (uint32_t r = KREG; r < R && !coll; ++r) {
-              uint32_t i = 32u * r + lane;
-              bool c = false;
-              if (i < k) {
-                uint32_t p = position(kl[i], g, m);
-                uint32_t bit = 1u << (p & 31);
-                c = (atomicOr(scr + (p >> 5), bit) & bit) != 0;
-              }
-              coll = __any_sync(FULL, c);
-            }
-            __syncwarp();
-            for (uint32_t w = lane; w < scr_used; w += 32) scr[w] = 0;
-            __syncwarp();
-          }
-          if (s == 0) {
-            // duplicate low words collide at every s, so they can only
-            // exist if s = 0 collides (_kernels.py:312-319)
-            if (coll) {
-              bool dup = false;
-              if (k <= 32) {
-                uint32_t peers = __match_any_sync(FULL, key[0]) & amask;
-                dup = lane < (int)k && __popc(peers) > 1;
-              } else if (R <= (uint32_t)KREG) {
-#pragma unroll
-                for (int r1 = 0; r1 < KREG; ++r1) {
-                  if ((uint32_t)r1 < R) {
-                    const uint32_t kr = min(32u, k - 32u * r1);
-                    for (uint32_t src = 0; src < kr; ++src) {
-                      uint64_t v = __shfl_sync(FULL, key[r1], src);
-#pragma unroll
-                      for (int r2 = 0; r2 < KREG; ++r2) {
-                        uint32_t i2 = 32u * r2 + lane;
-                        if ((uint32_t)r2 < R && i2 < k && i2 != 32u * r1 + src && key[r2] == v)
-                          dup = true;
-                      }
-                    }
-                  }
-                }
-              } else {
-                for (uint32_t i = 0; i < k; ++i) {
-                  uint64_t v = kl[i];
-                  for (uint32_t i2 = lane; i2 < k; i2 += 32)
-                    if (i2 != i && kl[i2] == v) dup = true;
-                }
-              }
-              if (__any_sync(FULL, dup)) {
-                status = 1;
-                break;
-              }
-            }
-            if (pbase > cap) {
-              status = 2;
-              break;
-            }
-          }
-          if (coll) {
-            trials += k;
-            continue;
-          }
-          int64_t dmax = cap - pbase;
-          if (dmax > (int64_t)m - 1) dmax = (int64_t)m - 1;
-          int64_t d = first_valid(occ, pos, k, dmax, kl, g, m, lane);
-          if (d >= 0) {
-            trials += (int64_t)k * (d + 1);
-            seed = pbase + d;
-#pragma unroll
-            for (int r = 0; r < KREG; ++r) {
-              uint32_t i = 32u * r + lane;
-              if ((uint32_t)r < R && i < k) {
-                uint32_t slot = pos[r] + (uint32_t)d;
-                if (slot >= m) slot -= m;
-                mark(occ, slot, m);
-              }
-            }
-            for (uint32_t r = KREG; r < R; ++r) {
-              uint32_t i = 32u * r + lane;
-              if (i < k) {
-                uint32_t slot = position(kl[i], g, m) + (uint32_t)d;
-                if (slot >= m) slot -= m;
-                mark(occ, slot, m);
-              }
-            }
-            break;
-          }
-          trials += (int64_t)k * (dmax + 1);
-        }
-        if (status) break;
+        res = generic_bucket(occ, scr, pos16, k, kl, m, cap, 0, 0, lane);
+      }
+      if (res.status > 0) {
+        status = (uint8_t)res.status;
+        break;
       }
       __syncwarp();
       if (lane == 0) {
-        a.seeds[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = (uint64_t)seed;
-        if (a.trials) a.trials[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = trials;
+        a.seeds[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = (uint64_t)res.seed;
+        if (a.trials) a.trials[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = res.trials;
       }
-      ptrials += trials;
+      ptrials += res.trials;
     }
     __syncwarp();
     if (lane == 0) {
@@ -424,6 +533,7 @@ int launch_search(const SearchArgs& a, cudaStream_t st) {
   const int64_t nrange = a.p_hi - a.p_lo;
   if (nrange <= 0) return 0;
   if (a.bcount < 1 || a.bcount > 65535) return 1001;  // PHB_E_BUCKETS
+  if (a.m_max >= 65536) return 1002;                   // u16 positions
   SmemPlan plan = smem_plan(a.m_max < 1 ? 1 : a.m_max, a.bcount);
   size_t per_cta = (size_t)plan.total_w * 4 * WARPS;
   int dev = 0;
