@@ -13,8 +13,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "_obj"
-LIB = PKG / "libphobic_b200.so"
+OBJ = Path(os.environ["PHB_OBJ"]) if os.environ.get("PHB_OBJ") else PKG / "_obj"
+LIB = Path(os.environ["PHB_LIB"]) if os.environ.get("PHB_LIB") else PKG / "libphobic_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = os.environ.get("PHB_NVCC_EXTRA", "").split() + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",

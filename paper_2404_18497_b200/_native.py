@@ -12,7 +12,9 @@ from pathlib import Path
 
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "libphobic_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("PHB_LIB") or Path(__file__).resolve().parent / "libphobic_b200.so")
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32

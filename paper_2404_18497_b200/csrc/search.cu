@@ -34,6 +34,27 @@
 
 namespace phb {
 
+#ifndef PHB_LDS128
+#define PHB_LDS128 0  // measured slower (round 1): 4-way switch + code size
+#endif
+#ifndef PHB_MASKTAB
+#define PHB_MASKTAB 1
+#endif
+#ifndef PHB_IMADFUN
+#define PHB_IMADFUN 0
+#endif
+#ifndef PHB_USE_G2
+#define PHB_USE_G2 1
+#endif
+#ifndef PHB_NOINLINE_GENERIC
+#define PHB_NOINLINE_GENERIC 0
+#endif
+#if PHB_NOINLINE_GENERIC
+#define PHB_COLD __noinline__
+#else
+#define PHB_COLD
+#endif
+
 constexpr int SH = 256;     // size classes of the counting-sort bucket order
 constexpr int PMAX = 256;   // bucket sizes whose base positions are staged in smem
 constexpr int WARPS = 4;    // warps (= partitions in flight) per CTA
@@ -53,8 +74,9 @@ __host__ __device__ inline SmemPlan smem_plan(int64_t m_max, uint32_t bcount) {
   p.ord_w = (int)(bcount + 2) / 2;
   p.sh_w = SH;       // shist + srun as u16
   p.pos_w = PMAX / 2;  // u16 base positions
-  p.total_w = p.occ_w + p.scr_w + 2 * p.cnt_w + p.ord_w + p.sh_w + p.pos_w;
-  p.total_w += p.total_w & 1;
+  p.occ_w = (p.occ_w + 3) & ~3;  // keep the mask table that follows 16-byte aligned
+  p.total_w = p.occ_w + 96 + p.scr_w + 2 * p.cnt_w + p.ord_w + p.sh_w + p.pos_w;
+  p.total_w = (p.total_w + 3) & ~3;  // 16-byte aligned warp regions (LDS.128)
   return p;
 }
 
@@ -153,7 +175,7 @@ __device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_
 // First displacement d in [0, dmax] with every key's slot free, or -1.
 // Base positions come from the staged u16 list (k <= PMAX) or are re-derived
 // from the key scratch (larger buckets).
-__device__ __forceinline__ int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t k,
+__device__ PHB_COLD int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t k,
                                           int64_t dmax, const uint64_t* kl, uint64_t g,
                                           uint32_t m, int lane) {
   const uint32_t nwd = (uint32_t)((dmax + 32) >> 5);  // words of the valid mask
@@ -200,7 +222,7 @@ struct BucketResult {
 
 // Generic single-s search (any k, any m): the reference loop of
 // _kernels.py:312-369 with each s tested by the whole warp.
-__device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos16, uint32_t k,
+__device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos16, uint32_t k,
                                        const uint64_t* kl, uint32_t m, int64_t cap,
                                        int64_t s_begin, int64_t trials, int lane) {
   const uint32_t R = (k + 31) >> 5;
@@ -293,6 +315,32 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
   }
 }
 
+// acc[t] |= window of 32 occupancy bits starting at bit 32*(R+t) + sh of w.
+// The ALU pipe (SHF, LOP3) is the binding unit of the search, so two of
+// every three windows are formed on the FMA pipe instead: with
+// P = 2^(32 - sh), (x >> sh) | (y << (32 - sh)) == hi(x * P) + lo(y * P).
+template <int R, int WPL>
+__device__ __forceinline__ void accumulate(uint32_t (&acc)[WPL], const uint32_t (&w)[16],
+                                           uint32_t sh) {
+  if (sh == 0) {
+#pragma unroll
+    for (int t = 0; t < WPL; ++t) acc[t] |= w[R + t];
+    return;
+  }
+  const uint32_t P = 1u << (32 - sh);
+#pragma unroll
+  for (int t = 0; t < WPL; ++t) {
+    uint32_t win;
+    if (!PHB_IMADFUN || t % 3 == 0) {
+      win = __funnelshift_r(w[R + t], w[R + t + 1], sh);
+    } else {
+      const uint32_t h = __umulhi(w[R + t], P);
+      win = w[R + t + 1] * P + h;
+    }
+    acc[t] |= win;
+  }
+}
+
 // Batched search for small buckets (k <= 32 / G) in partitions with
 // m <= 3072: G consecutive seeds s are tested per step, one group of
 // L = 32 / G lanes per seed, each lane owning WPL = 96 / L consecutive
@@ -301,7 +349,7 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
 // loop, so seeds and trials are unchanged. Returns status -1 when
 // max_batches ran out without a decision (the caller continues).
 template <int G>
-__device__ BucketResult small_bucket(uint32_t occ, uint16_t* pos16, uint32_t k,
+__device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos16, uint32_t k,
                                      const uint64_t* kl, uint32_t m, int64_t cap,
                                      int64_t& s_next, int64_t trials, int max_batches,
                                      int lane) {
@@ -339,19 +387,50 @@ __device__ BucketResult small_bucket(uint32_t occ, uint16_t* pos16, uint32_t k,
     if (dmax > (int64_t)m - 1) dmax = (int64_t)m - 1;
     uint32_t acc[WPL];
     const bool dead_group = gcoll || gcap;
-#pragma unroll
-    for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : 0u;
     const uint32_t wb = (uint32_t)gl * WPL;
-    for (uint32_t i = 0; i < k; ++i) {
-      const uint32_t pi = mypos[i];
-      const uint32_t W = occ + (pi >> 5) + wb;
-      const uint32_t sh = pi & 31;
-      uint32_t x = smem[W];
+    // start from "displacements past dmax are occupied": the partition's
+    // mask table (dmax = m - 1) or, near the seed cap, computed here
+    if (PHB_MASKTAB && dmax == (int64_t)m - 1) {
+#pragma unroll
+      for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : smem[dmask + wb + t];
+    } else {
+      const int64_t lim = dmax - 32 * (int64_t)wb;
 #pragma unroll
       for (int t = 0; t < WPL; ++t) {
-        const uint32_t y = smem[W + t + 1];
-        acc[t] |= __funnelshift_r(x, y, sh);
-        x = y;
+        const int64_t lt = lim - 32 * t;
+        acc[t] = (dead_group || lt < 0) ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
+      }
+    }
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint32_t pi = mypos[i];
+      const uint32_t sh = pi & 31;
+      if constexpr (G == 4 && PHB_LDS128) {
+        // 8 lanes x 12 words: 16-byte aligned LDS.128 reads cover each lane's
+        // 13 words in 4 loads, conflict-free per quarter-warp (lanes 12*gl
+        // words apart tile all 32 banks); the word offset r = (p >> 5) & 3
+        // is warp-uniform, so the funnel shifts use static register indices.
+        const uint32_t A = occ + ((pi >> 5) & ~3u) + wb;
+        uint32_t w[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 q = *reinterpret_cast<const uint4*>(&smem[A + 4 * c]);
+          w[4 * c] = q.x, w[4 * c + 1] = q.y, w[4 * c + 2] = q.z, w[4 * c + 3] = q.w;
+        }
+        switch ((pi >> 5) & 3u) {
+          case 0: accumulate<0, WPL>(acc, w, sh); break;
+          case 1: accumulate<1, WPL>(acc, w, sh); break;
+          case 2: accumulate<2, WPL>(acc, w, sh); break;
+          default: accumulate<3, WPL>(acc, w, sh); break;
+        }
+      } else {
+        const uint32_t W = occ + (pi >> 5) + wb;
+        uint32_t x = smem[W];
+#pragma unroll
+        for (int t = 0; t < WPL; ++t) {
+          const uint32_t y = smem[W + t + 1];
+          acc[t] |= __funnelshift_r(x, y, sh);
+          x = y;
+        }
       }
       if ((i & 3) == 3) {
         uint32_t all = FULL;
@@ -361,16 +440,17 @@ __device__ BucketResult small_bucket(uint32_t occ, uint16_t* pos16, uint32_t k,
       }
     }
     // this lane's first valid displacement (d <= dmax), or -1
-    int64_t myd = -1;
-    const int64_t lim = dmax - 32 * (int64_t)wb;
+    uint32_t sat = FULL;
 #pragma unroll
-    for (int t = WPL - 1; t >= 0; --t) {
-      uint32_t v = ~acc[t];
-      const int64_t lt = lim - 32 * t;
-      v = lt < 0 ? 0u : (lt < 31 ? v & ((2u << lt) - 1u) : v);
-      if (v) myd = 32 * (int64_t)(wb + t) + (__ffs(v) - 1);
+    for (int t = 0; t < WPL; ++t) sat &= acc[t];
+    const bool hv = sat != FULL;
+    const uint32_t fball = __ballot_sync(FULL, hv);
+    int64_t myd = -1;
+    if (hv) {
+#pragma unroll
+      for (int t = WPL - 1; t >= 0; --t)
+        if (acc[t] != FULL) myd = 32 * (int64_t)(wb + t) + (__ffs(~acc[t]) - 1);
     }
-    const uint32_t fball = __ballot_sync(FULL, myd >= 0);
     // resolve the G seeds in order, like the sequential loop
     for (int gi = 0; gi < G; ++gi) {
       const int64_t si = s_next + gi;
@@ -415,7 +495,8 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t B = a.bcount;
   const uint32_t occ = wid * plan.total_w;
-  const uint32_t scr = occ + plan.occ_w;
+  const uint32_t dmask = occ + plan.occ_w;  // 96-word "past dmax" table for dmax = m - 1
+  const uint32_t scr = dmask + 96;
   const uint32_t cnt = scr + plan.scr_w;
   const uint32_t endp = cnt + plan.cnt_w;
   uint16_t* const sm16 = reinterpret_cast<uint16_t*>(smem);
@@ -469,6 +550,10 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
     for (uint32_t w = lane; w < occ_used; w += 32) smem[occ + w] = 0;
     const uint32_t scr_used = m / 32 + 2;
     for (uint32_t w = lane; w < scr_used; w += 32) smem[scr + w] = 0;
+    for (uint32_t w = lane; w < 96; w += 32) {
+      const int64_t lt = (int64_t)m - 1 - 32 * (int64_t)w;  // last valid bit of word w
+      smem[dmask + w] = lt < 0 ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
+    }
     __syncwarp();
 
     const uint32_t nb = bucket_order(cnt, B, a.tie_desc, maxsz, order, shist, srun, lane);
@@ -496,16 +581,19 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
         res = {d, d + 1, 0};
       } else if (small_ok && k <= 32) {
         // one single-seed step first (sparse tables usually succeed at s = 0),
-        // then batches of G seeds
+        // then batches of G seeds; one call site per instantiation keeps the
+        // kernel's instruction footprint small
         int64_t s_next = 0;
-        res = small_bucket<1>(occ, pos16, k, kl, m, cap, s_next, 0, 1, lane);
+        const uint32_t kg1 = PHB_USE_G2 ? 16u : 8u;  // larger buckets stay single-seed
+        res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, 0, k > kg1 ? (1 << 30) : 1,
+                              lane);
         if (res.status < 0) {
           if (k <= 8)
-            res = small_bucket<4>(occ, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
-          else if (k <= 16)
-            res = small_bucket<2>(occ, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+            res = small_bucket<4>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+#if PHB_USE_G2
           else
-            res = small_bucket<1>(occ, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+            res = small_bucket<2>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+#endif
         }
       } else {
         res = generic_bucket(occ, scr, pos16, k, kl, m, cap, 0, 0, lane);

@@ -163,18 +163,19 @@ class BuildEngine:
 
 
 class Mphf:
-    def __init__(self, global_seed: int, layout: PartitionLayout, table: AssignmentTable,
-                 bcount: int, seeds: SeedStore, lambda_: float, partition_size: float,
+    def __init__(self, global_seed: int, layout: PartitionLayout | None, table: AssignmentTable,
+                 bcount: int, seeds: SeedStore | None, lambda_: float, partition_size: float,
                  stats: BuildStats | None = None):
         self.global_seed = global_seed
-        self.layout = layout
+        self._layout = layout
         self.table = table
         self.bcount = bcount
-        self.seeds = seeds
+        self._seeds = seeds
         self.lambda_ = lambda_
         self.partition_size = partition_size
         self.stats = stats
-        self._body: bytes | None = None  # serialized body without checksum
+        self._body = None  # serialized body without checksum (bytes-like)
+        self._dev = None   # DeviceBuild backing a freshly built structure
         self._dev_key_off: torch.Tensor | None = None
         self._dev_entries: torch.Tensor | None = None
 
@@ -182,27 +183,56 @@ class Mphf:
     @classmethod
     def _from_device(cls, db: DeviceBuild, config: BuildConfig, engine: BuildEngine,
                      stats: BuildStats) -> "Mphf":
-        body = bytearray(db.blob[: db.total_bytes].cpu().numpy().tobytes())
-        head = _header(db.n, db.nparts, config.lambda_, config.partition_size, engine.spec,
-                       db.global_seed)
-        body[:HEADER_FIXED] = head
-        body = bytes(body)
-        deltas = db.deltas.cpu().numpy()
-        deltas.setflags(write=False)
-        layout = PartitionLayout(db.n, db.nparts, deltas)
-        store, _ = parse_section(body, db.seed_section, db.nparts, db.bcount)
-        store._device = db.seeds.view(db.bcount, db.nparts)
-        f = cls(db.global_seed, layout, engine.table, db.bcount, store, config.lambda_,
+        """Wrap a device build. The only eager host work is one D2H of the
+        encoded body into pinned memory (the build's result); the layout and
+        the seed-store views over the bytes are materialised on first use."""
+        host = torch.empty(db.total_bytes, dtype=torch.uint8, pin_memory=True)
+        host.copy_(db.blob[: db.total_bytes], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        body = host.numpy()
+        body[:HEADER_FIXED] = np.frombuffer(
+            _header(db.n, db.nparts, config.lambda_, config.partition_size, engine.spec,
+                    db.global_seed), np.uint8)
+        f = cls(db.global_seed, None, engine.table, db.bcount, None, config.lambda_,
                 config.partition_size, stats)
         f._body = body
+        f._body_owner = host
+        f._dev = db
         f._dev_key_off = db.key_off
         f._dev_entries = engine.entries
         return f
 
+    @property
+    def layout(self) -> PartitionLayout:
+        if self._layout is None:
+            db = self._dev
+            deltas = db.deltas.cpu().numpy()
+            deltas.setflags(write=False)
+            self._layout = PartitionLayout(db.n, db.nparts, deltas)
+        return self._layout
+
+    @layout.setter
+    def layout(self, value: PartitionLayout) -> None:
+        self._layout = value
+
+    @property
+    def seeds(self) -> SeedStore:
+        if self._seeds is None:
+            db = self._dev
+            store, _ = parse_section(memoryview(self._body), db.seed_section, db.nparts,
+                                     db.bcount)
+            store._device = db.seeds.view(db.bcount, db.nparts)
+            self._seeds = store
+        return self._seeds
+
+    @seeds.setter
+    def seeds(self, value: SeedStore) -> None:
+        self._seeds = value
+
     # ---- properties -----------------------------------------------------
     @property
     def n(self) -> int:
-        return self.layout.n
+        return self._dev.n if self._layout is None else self._layout.n
 
     @property
     def encoder_name(self) -> str:
@@ -218,6 +248,8 @@ class Mphf:
     # ---- query ----------------------------------------------------------
     def _device_state(self):
         dev = _native.require_device()
+        if self._dev is not None:
+            return self._dev_key_off, self._dev_entries, self._dev.seeds
         if self._dev_key_off is None:
             d = torch.from_numpy(np.ascontiguousarray(self.layout.deltas, np.int64)).to(dev)
             key_off = torch.empty(self.layout.num_partitions + 1, dtype=torch.int64, device=dev)
@@ -227,6 +259,10 @@ class Mphf:
         if self._dev_entries is None:
             self._dev_entries = device_table(self.table, dev)
         return self._dev_key_off, self._dev_entries, self.seeds.device_matrix()
+
+    @property
+    def num_partitions(self) -> int:
+        return self._dev.nparts if self._layout is None else self._layout.num_partitions
 
     def query_device(self, keys) -> torch.Tensor:
         """Batched device query -> int64 CUDA tensor (query_many_kernel, _kernels.py:379-397)."""
@@ -238,8 +274,8 @@ class Mphf:
         _native.call("phb_query", None if dk.is_u64 else P(dk.buf),
                      None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
                      dk.n, self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n,
-                     self.layout.num_partitions, P(key_off), P(entries), self.bcount, P(seeds),
-                     1, self.layout.num_partitions, P(out), _native.stream())
+                     self.num_partitions, P(key_off), P(entries), self.bcount, P(seeds),
+                     1, self.num_partitions, P(out), _native.stream())
         return out
 
     def query_many(self, keys) -> np.ndarray:
@@ -282,7 +318,7 @@ class Mphf:
 
     def serialize(self) -> bytes:
         body = self._serialized_body()
-        return body + struct.pack("<Q", _checksum(body))
+        return bytes(body) + struct.pack("<Q", _checksum(body))
 
     def save(self, path) -> None:
         with open(path, "wb") as f:
