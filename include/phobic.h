@@ -163,6 +163,15 @@ int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint
 int phb_offsets_from_deltas(const int64_t* deltas, int64_t n, int64_t nparts, int64_t* key_off,
                             void* stream);
 
+/* Multi-GPU regroup (paper_2404_18497_b200/distributed.py): merge the G
+ * chunks received from the all-to-all, each grouped by the owned partitions
+ * [0, np) with C[s*np + j] records of partition j from source s (int32,
+ * row-major [G][np]), into one partition-grouped array; key_off[np+1] gets
+ * the partition offsets. No reference counterpart (the reference is single
+ * process). */
+int phb_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t* counts, int64_t G,
+                int64_t np, uint64_t* lo_out, uint16_t* aux_out, int64_t* key_off, void* stream);
+
 /* Synthetic distinct 64-bit keys for benchmarks: out[i] = mix64(offset + i)
  * (mix64 is a bijection on u64, so keys are distinct for distinct i). The
  * host restatement is keygen.synth_u64. Not a reference interface: bench

@@ -42,6 +42,7 @@ SIGNATURES = {
     "phb_offsets_from_deltas": [P, I64, I64, P, P],
     "phb_device_sms": [],
     "phb_synth_keys": [P, I64, U64, P],
+    "phb_regroup": [P, P, P, I64, I64, P, P, P, P],
 }
 OTHER = {
     "phb_version": ([], ctypes.c_char_p),

@@ -305,6 +305,11 @@ int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint
   return launch_verify(out, nq, n, bitmap, bad_flag, S(stream));
 }
 
+int phb_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t* counts, int64_t G,
+                int64_t np, uint64_t* lo_out, uint16_t* aux_out, int64_t* key_off, void* stream) {
+  return launch_regroup(lo_in, aux_in, counts, G, np, lo_out, aux_out, key_off, S(stream));
+}
+
 int phb_synth_keys(uint64_t* out, int64_t n, uint64_t offset, void* stream) {
   if (n < 0) return PHB_E_ARGS;
   if (n == 0) return 0;

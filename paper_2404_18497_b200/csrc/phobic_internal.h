@@ -30,6 +30,10 @@ int launch_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int6
                   int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                   int64_t* stats, void* temp, size_t temp_bytes, cudaStream_t st);
 
+int launch_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t* C, int64_t G,
+                   int64_t np, uint64_t* lo_out, uint16_t* aux_out, int64_t* key_off,
+                   cudaStream_t st);
+
 // search.cu
 struct SearchArgs {
   const uint64_t* lo;

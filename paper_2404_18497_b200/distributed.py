@@ -1,0 +1,255 @@
+"""Multi-GPU PHOBIC construction: one process per GPU, NCCL over NVLink.
+
+SURVEY.md §8(e). The result is independent of the number of ranks G: every
+quantity that defines the MPHF (n, nparts, partition index, bucket ids,
+partition offsets, seeds) is global, and the bytes equal those of a
+single-GPU build over the concatenated keys.
+
+Per attempt (global_seed + attempt, the reference's retry, mphf.py:251-261):
+  1. K1 on the local shard: per-partition counts over the GLOBAL nparts.
+  2. all_gather of the count vectors -> C[s][j] (G x nparts int32). Every
+     rank derives the global layout (key offsets, deltas, max |delta|).
+  3. K3 on the local shard, grouped by partition with local offsets: since
+     j = mulhi(hi, nparts) is monotone in hi and rank g owns the contiguous
+     partition range [g*nparts/G, (g+1)*nparts/G), the local records are
+     also grouped by destination rank.
+  4. all_to_all_single of the (lo, bucket-id) records: 10 B/key, no
+     re-hashing at the destination (string keys never move).
+  5. regroup: the G received chunks (each partition-sorted) are merged into
+     one partition-grouped array (a segmented copy, phb_regroup).
+  6. K4 search on the owned partitions; all_reduce of the failure flag
+     (collective retry) and of the trial count.
+  7. all_gather of the owned seed columns -> every rank assembles the global
+     [B][nparts] seed matrix and runs K5 (replicated; the encoded body is
+     identical on every rank), so every rank holds a queryable Mphf.
+
+The kernels are reached through an ``ops`` object. ``DeviceOps`` (default)
+calls the C-ABI; the CPU tests inject an oracle-backed implementation to
+check this orchestration with the gloo backend (tests/test_distributed.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native
+from .builder import BuildConfig, InvalidConfig, SeedExhausted, device_table
+from .keygen import DeviceKeys, to_device
+from .partitioning import num_partitions_for
+
+MAX_ATTEMPTS = 4
+
+
+def owner_bounds(nparts: int, world: int) -> list[int]:
+    """Partition range of rank g is [b[g], b[g+1]) (contiguous, balanced)."""
+    return [g * nparts // world for g in range(world + 1)]
+
+
+class DeviceOps:
+    """The C-ABI kernels (paper_2404_18497_b200/csrc), one CUDA stream."""
+
+    aux_dtype = torch.int16  # bucket ids travel with the low words
+
+    def __init__(self, config: BuildConfig):
+        from .assignment import tabulate
+
+        self.config = config
+        self.dev = _native.require_device()
+        self.spec = config.resolved_assignment()
+        self.table = tabulate(self.spec)
+        self.entries = device_table(self.table, self.dev)
+        self.B = config.bucket_count
+
+    def stage(self, keys) -> DeviceKeys:
+        return to_device(keys, self.dev)
+
+    def hash_count(self, dk: DeviceKeys, seed: int, nparts: int) -> torch.Tensor:
+        counts = torch.zeros(nparts, dtype=torch.int32, device=self.dev)
+        P = _native.ptr
+        _native.call("phb_hash_count", None if dk.is_u64 else P(dk.buf),
+                     None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
+                     dk.n, seed, nparts, P(counts), _native.stream())
+        return counts
+
+    def layout(self, counts: torch.Tensor, n: int, nparts: int):
+        key_off = torch.empty(nparts + 1, dtype=torch.int64, device=self.dev)
+        deltas = torch.empty(nparts + 1, dtype=torch.int64, device=self.dev)
+        stats = torch.empty(2, dtype=torch.int64, device=self.dev)
+        P = _native.ptr
+        _native.call("phb_layout", P(counts), nparts, 0, 0, n, nparts, P(key_off), P(deltas),
+                     P(stats), _native.stream())
+        return key_off, deltas, stats
+
+    def scatter(self, dk: DeviceKeys, seed: int, nparts: int, key_off: torch.Tensor):
+        cursor = torch.zeros(nparts, dtype=torch.int32, device=self.dev)
+        lo = torch.empty(dk.n, dtype=torch.int64, device=self.dev)
+        aux = torch.empty(dk.n, dtype=torch.int16, device=self.dev)
+        P = _native.ptr
+        _native.call("phb_scatter", None if dk.is_u64 else P(dk.buf),
+                     None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
+                     dk.n, seed, nparts, P(self.entries), self.B, P(key_off), P(cursor), P(lo),
+                     P(aux), _native.stream())
+        return lo, aux
+
+    def regroup(self, lo_recv, aux_recv, C_owned: torch.Tensor, recv_splits):
+        """Merge G partition-sorted chunks into one partition-grouped array."""
+        G, np_g = C_owned.shape
+        n = lo_recv.numel()
+        lo = torch.empty(n, dtype=torch.int64, device=self.dev)
+        aux = torch.empty(n, dtype=torch.int16, device=self.dev)
+        key_off = torch.empty(np_g + 1, dtype=torch.int64, device=self.dev)
+        C = C_owned.to(self.dev, torch.int32).contiguous()
+        P = _native.ptr
+        _native.call("phb_regroup", P(lo_recv), P(aux_recv), P(C), G, np_g, P(lo), P(aux),
+                     P(key_off), _native.stream())
+        return lo, aux, key_off
+
+    def search(self, lo, aux, key_off, np_g: int, m_max: int):
+        B = self.B
+        seeds = torch.zeros(B * np_g, dtype=torch.int64, device=self.dev)
+        part_trials = torch.empty(np_g, dtype=torch.int64, device=self.dev)
+        status = torch.empty(np_g, dtype=torch.uint8, device=self.dev)
+        glo = torch.empty(max(lo.numel(), 1), dtype=torch.int64, device=self.dev)
+        queue = torch.empty(1, dtype=torch.int32, device=self.dev)
+        P = _native.ptr
+        cfg = self.config
+        _native.call("phb_search", P(lo), P(aux), P(key_off), 0, np_g, 0, B, cfg.seed_cap,
+                     cfg.tie_desc, m_max, P(seeds), 1, np_g, None, P(part_trials), P(status),
+                     P(glo), P(queue), _native.stream())
+        return seeds.view(B, np_g), part_trials, status
+
+    def encode(self, seeds_cm: torch.Tensor, deltas, stats, nparts: int):
+        """K5 over the global column-major seed matrix -> (blob, summary)."""
+        mono, prefix = self.config.compact_prefix()
+        B = self.B
+        L = _native.lib()
+        P = _native.ptr
+        ws = torch.empty(int(L.phb_encode_workspace_bytes(nparts, B, mono)), dtype=torch.uint8,
+                         device=self.dev)
+        summ = np.zeros(8, np.int64)
+        seeds_cm = seeds_cm.contiguous()
+        _native.call("phb_encode_plan", P(seeds_cm), nparts, B, mono, prefix, P(deltas), nparts,
+                     P(stats), None, None, P(ws), summ.ctypes.data_as(ctypes.c_void_p),
+                     _native.stream())
+        total = int(summ[0])
+        blob = torch.empty((total + 16 + 3) // 4 * 4, dtype=torch.uint8, device=self.dev)
+        _native.call("phb_encode_write", P(seeds_cm), nparts, B, mono, prefix, P(deltas),
+                     nparts, P(stats), P(ws), P(blob), blob.numel(), _native.stream())
+        return blob, summ
+
+
+def _as_bytes(t: torch.Tensor) -> torch.Tensor:
+    return t.contiguous().view(torch.uint8)
+
+
+def build_distributed(local_keys, config: BuildConfig | None = None, group=None, ops=None,
+                      to_host: bool = True):
+    """Collective build: every rank passes its shard; every rank returns the
+    same Mphf (global n, identical bytes for any world size). With
+    to_host=False the device-resident DeviceBuild is returned instead."""
+    from .mphf import BuildStats, DeviceBuild, DuplicateKeys, Mphf
+
+    config = config or BuildConfig()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ops = ops or DeviceOps(config)
+    t0 = time.perf_counter()
+    dk = ops.stage(local_keys)
+    comm_dev = getattr(ops, "comm_device", None) or (ops.dev if hasattr(ops, "dev") else "cpu")
+    n_t = torch.tensor([dk.n], dtype=torch.int64, device=comm_dev)
+    dist.all_reduce(n_t, group=group)
+    n = int(n_t.item())
+    if n < 1:
+        raise InvalidConfig("need at least one key")
+    nparts = num_partitions_for(n, config.partition_size)
+    bounds = owner_bounds(nparts, world)
+    p_lo, p_hi = bounds[rank], bounds[rank + 1]
+    np_g = p_hi - p_lo
+    last = None
+    for attempt in range(MAX_ATTEMPTS):
+        seed = (config.global_seed + attempt) & 0xFFFFFFFFFFFFFFFF
+        # 1-2. local counts, all_gather -> C[s][j]
+        counts = ops.hash_count(dk, seed, nparts)
+        gathered = [torch.empty_like(counts) for _ in range(world)]
+        dist.all_gather(gathered, counts, group=group)
+        C = torch.stack(gathered).to(torch.int64)            # [G, nparts]
+        total_counts = C.sum(0).to(torch.int32)
+        key_off_g, deltas, stats = ops.layout(total_counts, n, nparts)
+        # 3. group own keys by partition (hence by destination rank)
+        key_off_l = torch.zeros(nparts + 1, dtype=torch.int64, device=C.device)
+        torch.cumsum(C[rank], 0, out=key_off_l[1:])
+        lo, aux = ops.scatter(dk, seed, nparts, key_off_l)
+        kb = key_off_l[torch.tensor(bounds, device=C.device)].cpu().tolist()
+        send = [kb[g + 1] - kb[g] for g in range(world)]
+        C_owned = C[:, p_lo:p_hi]
+        recv = C_owned.sum(1).cpu().tolist()
+        # 4. all-to-all of the records (byte views: gloo/NCCL-safe dtypes)
+        esz = aux.element_size()
+        lo_r = torch.empty(sum(recv), dtype=lo.dtype, device=lo.device)
+        aux_r = torch.empty(sum(recv) * esz, dtype=torch.uint8, device=lo.device)
+        dist.all_to_all_single(lo_r, lo, recv, send, group=group)
+        dist.all_to_all_single(aux_r, _as_bytes(aux), [r * esz for r in recv],
+                               [s * esz for s in send], group=group)
+        aux_r = aux_r.view(aux.dtype)
+        # 5. merge the G partition-sorted chunks
+        lo_g, aux_g, key_off_own = ops.regroup(lo_r, aux_r, C_owned, recv)
+        m_max = int(C_owned.sum(0).max().item()) if np_g else 0
+        # 6. search + collective failure / trials
+        if np_g:
+            seeds_own, part_trials, status = ops.search(lo_g, aux_g, key_off_own, np_g, m_max)
+            st = status.to(torch.int64)
+            bad_local = (torch.nonzero(st).flatten()[:1] + p_lo)
+            bad = int(bad_local.item()) if bad_local.numel() else nparts
+            code = int(st[bad - p_lo].item()) if bad < nparts else 0
+            trials = int(part_trials.sum().item())
+        else:
+            seeds_own = torch.zeros((config.bucket_count, 0), dtype=torch.int64, device=C.device)
+            bad, code, trials = nparts, 0, 0
+        flag = torch.tensor([bad, trials], dtype=torch.int64, device=C.device)
+        red = flag.clone()
+        dist.all_reduce(red[0:1], op=dist.ReduceOp.MIN, group=group)
+        dist.all_reduce(red[1:2], op=dist.ReduceOp.SUM, group=group)
+        gbad = int(red[0].item())
+        if gbad < nparts:
+            code_t = torch.tensor([code if bad == gbad else 0], dtype=torch.int64, device=C.device)
+            dist.all_reduce(code_t, op=dist.ReduceOp.MAX, group=group)
+            reason = "unseparable duplicate hashes" if int(code_t.item()) == 1 else "seed cap hit"
+            last = f"partition {gbad}: {reason}"
+            continue
+        trials_total = int(red[1].item())
+        # 7. all_gather the owned seed columns (padded to the widest range)
+        B = config.bucket_count
+        width = max(bounds[g + 1] - bounds[g] for g in range(world))
+        pad = torch.zeros((B, width), dtype=torch.int64, device=seeds_own.device)
+        pad[:, :np_g] = seeds_own
+        blocks = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(blocks, pad, group=group)
+        seeds_cm = torch.cat([blocks[g][:, : bounds[g + 1] - bounds[g]] for g in range(world)], 1)
+        blob, summ = ops.encode(seeds_cm, deltas, stats, nparts)
+        stats_obj = BuildStats(attempt + 1, trials_total, trials_total / n,
+                               time.perf_counter() - t0)
+        if not isinstance(ops, DeviceOps):
+            return ops.finish(blob, summ, seed, n, nparts, deltas, seeds_cm, stats_obj)
+        db = DeviceBuild(n, nparts, B, seed, key_off_g, deltas, seeds_cm.reshape(-1), blob,
+                         int(summ[0]), int(summ[1]), trials_total)
+        if not to_host:
+            return db
+        eng = _EngineView(ops)
+        return Mphf._from_device(db, config, eng, stats_obj)
+    raise DuplicateKeys(
+        f"construction failed after {MAX_ATTEMPTS} seeds ({SeedExhausted(last)}); "
+        "input most likely contains duplicate keys")
+
+
+class _EngineView:
+    """The attributes of BuildEngine that Mphf._from_device reads."""
+
+    def __init__(self, ops: DeviceOps):
+        self.spec = ops.spec
+        self.table = ops.table
+        self.entries = ops.entries
