@@ -100,8 +100,8 @@ int phb_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int64_t
                int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                int64_t* stats, void* stream);
 
-/* K3: re-hash and scatter (lo, bucket id) into partition ranges (cursor[]
- * zeroed by caller). Replaces the lexsort grouping (partitioning.py:93-95)
+/* K3: re-hash and scatter (lo, bucket id) into partition ranges (cursor:
+ * nparts u32 of scratch, contents ignored; n < 2^32). Replaces the lexsort grouping (partitioning.py:93-95)
  * and _bucket_of (_kernels.py:252-255). */
 int phb_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
                 uint64_t seed, int64_t nparts, const double* entries, int32_t bcount,

@@ -12,6 +12,8 @@
 //
 // Both passes are HBM-bound streaming kernels: one thread per key, grid
 // sized in multiples of the SM count, coalesced 8-byte key loads.
+#include <algorithm>
+
 #include "common.cuh"
 #include "phobic_internal.h"
 
@@ -74,15 +76,14 @@ __global__ void __launch_bounds__(256) k_hash_count(K keys, int64_t n, uint64_t 
 }
 
 // K3: re-hash, compute the bucket id, and scatter (lo, bucket) into the
-// partition's contiguous range. Per-partition cursors advance
+// partition's contiguous range. cursor[j] starts at key_off[j] (absolute),
+// so one atomic gives the destination. Per-partition cursors advance
 // sequentially, so only ~nparts 32-byte sectors are write-active at a time
 // and L2 merges the scattered 8/2-byte stores into full sectors.
 template <class K>
 __global__ void __launch_bounds__(256) k_scatter(K keys, int64_t n, uint64_t seed, uint64_t nparts,
                                                  const double* __restrict__ entries,
-                                                 uint32_t bcount,
-                                                 const int64_t* __restrict__ key_off,
-                                                 uint32_t* __restrict__ cursor,
+                                                 uint32_t bcount, uint32_t* __restrict__ cursor,
                                                  uint64_t* __restrict__ lo_out,
                                                  uint16_t* __restrict__ bid_out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -90,10 +91,86 @@ __global__ void __launch_bounds__(256) k_scatter(K keys, int64_t n, uint64_t see
     Hash128 h = keys.hash(i, seed);
     uint32_t j = (uint32_t)mulhi(h.hi, nparts);
     uint32_t b = bucket_of(entries, h.hi, bcount);
-    int64_t pos = __ldg(key_off + j) + atomicAdd(cursor + j, 1u);
+    uint32_t pos = atomicAdd(cursor + j, 1u);
     lo_out[pos] = h.lo;
     bid_out[pos] = (uint16_t)b;
   }
+}
+
+// u64 fast path: 4 keys per thread per step (two 16-byte loads), so four
+// independent hash -> atomic -> store chains are in flight per thread.
+__global__ void __launch_bounds__(256) k_scatter_u64x4(const ulonglong2* __restrict__ keys2,
+                                                       int64_t n, uint64_t seed, uint64_t nparts,
+                                                       const double* __restrict__ entries,
+                                                       uint32_t bcount,
+                                                       uint32_t* __restrict__ cursor,
+                                                       uint64_t* __restrict__ lo_out,
+                                                       uint16_t* __restrict__ bid_out) {
+  const int64_t nq = n >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = __ldg(keys2 + 2 * q), c = __ldg(keys2 + 2 * q + 1);
+    const uint64_t k[4] = {a.x, a.y, c.x, c.y};
+    uint32_t pos[4], b[4];
+    uint64_t lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const Hash128 h = murmur3_u64(k[e], seed);
+      lo[e] = h.lo;
+      b[e] = bucket_of(entries, h.hi, bcount);
+      pos[e] = atomicAdd(cursor + (uint32_t)mulhi(h.hi, nparts), 1u);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      lo_out[pos[e]] = lo[e];
+      bid_out[pos[e]] = (uint16_t)b[e];
+    }
+  }
+  // tail (n % 4 keys)
+  const int64_t t = (nq << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) {
+    const uint64_t* keys = reinterpret_cast<const uint64_t*>(keys2);
+    const Hash128 h = murmur3_u64(__ldg(keys + t), seed);
+    const uint32_t pos = atomicAdd(cursor + (uint32_t)mulhi(h.hi, nparts), 1u);
+    lo_out[pos] = h.lo;
+    bid_out[pos] = (uint16_t)bucket_of(entries, h.hi, bcount);
+  }
+}
+
+__global__ void k_cursor_init(const int64_t* __restrict__ key_off, int64_t nparts,
+                              uint32_t* __restrict__ cursor) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nparts;
+       j += (int64_t)gridDim.x * blockDim.x)
+    cursor[j] = (uint32_t)key_off[j];
+}
+
+// K1 u64 fast path with a shared-memory histogram over all partitions
+// (up to ~56k bins in 224 KB): one CTA of 1024 threads per SM, 4 keys per
+// thread per step, then one global atomic per (CTA, non-empty bin).
+__global__ void __launch_bounds__(1024, 1) k_hash_count_u64x4(const ulonglong2* __restrict__ keys2,
+                                                              int64_t n, uint64_t seed,
+                                                              uint64_t nparts,
+                                                              uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t hist[];
+  for (uint32_t t = threadIdx.x; t < nparts; t += blockDim.x) hist[t] = 0;
+  __syncthreads();
+  const int64_t nq = n >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = __ldg(keys2 + 2 * q), c = __ldg(keys2 + 2 * q + 1);
+    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(a.x, seed).hi, nparts), 1u);
+    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(a.y, seed).hi, nparts), 1u);
+    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(c.x, seed).hi, nparts), 1u);
+    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(c.y, seed).hi, nparts), 1u);
+  }
+  const int64_t t = (nq << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) {
+    const uint64_t* keys = reinterpret_cast<const uint64_t*>(keys2);
+    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(__ldg(keys + t), seed).hi, nparts), 1u);
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < nparts; j += blockDim.x)
+    if (hist[j]) atomicAdd(counts + j, hist[j]);
 }
 
 // Bucket ids of already-hashed, already-grouped keys (used by the
@@ -126,13 +203,26 @@ int launch_murmur(const uint8_t* buf, const int64_t* offsets, const uint64_t* ke
   return (int)cudaGetLastError();
 }
 
-constexpr uint64_t SMEM_HIST_MAX = 12288;  // 48 KB of u32 bins
+constexpr uint64_t SMEM_HIST_MAX = 12288;      // 48 KB of u32 bins (256-thread CTAs)
+constexpr uint64_t SMEM_HIST_MAX_BIG = 56 * 1024; // 224 KB (one 1024-thread CTA per SM)
+
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                       int64_t n, uint64_t seed, uint64_t nparts, uint32_t* counts,
                       cudaStream_t st) {
   if (n <= 0) return 0;
   int g = grid_for(n);
+  if (keys64 && aligned16(keys64) && nparts > SMEM_HIST_MAX && nparts <= SMEM_HIST_MAX_BIG) {
+    size_t sh = nparts * sizeof(uint32_t);
+    PHB_CUDA_TRY(cudaFuncSetAttribute(k_hash_count_u64x4,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+    int64_t need = ((n >> 2) + 1023) / 1024;
+    int gb = (int)std::max<int64_t>(1, std::min<int64_t>(need, num_sms()));
+    k_hash_count_u64x4<<<gb, 1024, sh, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n,
+                                            seed, nparts, counts);
+    return (int)cudaGetLastError();
+  }
   if (nparts <= SMEM_HIST_MAX) {
     // fewer, fatter CTAs: the flush costs nparts atomics per CTA
     int gs = g < 2 * num_sms() ? g : 2 * num_sms();
@@ -157,13 +247,22 @@ int launch_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
                    const int64_t* key_off, uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
                    cudaStream_t st) {
   if (n <= 0) return 0;
+  if (n >= (int64_t(1) << 32)) return 1003;  // u32 cursors
+  k_cursor_init<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+      key_off, (int64_t)nparts, cursor);
+  PHB_CUDA_TRY(cudaGetLastError());
   int g = grid_for(n);
-  if (keys64)
-    k_scatter<<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, entries, bcount, key_off,
-                                 cursor, lo_out, bid_out);
-  else
+  if (keys64 && aligned16(keys64)) {
+    int g4 = grid_for((n + 3) / 4);
+    k_scatter_u64x4<<<g4, 256, 0, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n, seed,
+                                        nparts, entries, bcount, cursor, lo_out, bid_out);
+  } else if (keys64) {
+    k_scatter<<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, entries, bcount, cursor,
+                                 lo_out, bid_out);
+  } else {
     k_scatter<<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, entries, bcount,
-                                 key_off, cursor, lo_out, bid_out);
+                                 cursor, lo_out, bid_out);
+  }
   return (int)cudaGetLastError();
 }
 

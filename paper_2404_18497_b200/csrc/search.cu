@@ -40,8 +40,11 @@ namespace phb {
 #ifndef PHB_MASKTAB
 #define PHB_MASKTAB 1
 #endif
-#ifndef PHB_IMADFUN
-#define PHB_IMADFUN 0
+#ifndef PHB_PAIR
+#define PHB_PAIR 0  // measured slower (round 1)
+#endif
+#ifndef PHB_FASTRES
+#define PHB_FASTRES 0  // measured slower (round 1): code size
 #endif
 #ifndef PHB_USE_G2
 #define PHB_USE_G2 1
@@ -119,8 +122,10 @@ __device__ __forceinline__ void mark(uint32_t occ, uint32_t slot, uint32_t m, in
 __device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_t maxsz,
                                  uint16_t* order, uint16_t* shist, uint16_t* srun, int lane) {
   if (maxsz < (uint32_t)SH) {
+#pragma unroll 1
     for (int s = lane; s < SH; s += 32) shist[s] = 0, srun[s] = 0;
     __syncwarp();
+#pragma unroll 1
     for (uint32_t c0 = 1; c0 <= B; c0 += 32) {
       uint32_t b = c0 + lane;
       uint32_t sz = b <= B ? smem[cnt + b] : 0u;
@@ -130,6 +135,7 @@ __device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_
     }
     // base[s] = number of buckets with size > s
     uint32_t run = 0;
+#pragma unroll 1
     for (int c = 0; c < SH / 32; ++c) {
       int s = SH - 1 - (c * 32 + lane);
       uint32_t v = shist[s];
@@ -139,6 +145,7 @@ __device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_
       run += __shfl_sync(FULL, inc, 31);
     }
     __syncwarp();
+#pragma unroll 1
     for (uint32_t c0 = 0; c0 < B; c0 += 32) {
       uint32_t idx = c0 + lane;
       uint32_t b = tie_desc ? (B - idx) : (idx + 1);
@@ -153,12 +160,14 @@ __device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_
   }
   // general path (some bucket holds >= SH keys): rank by direct comparison
   uint32_t nb = 0;
+#pragma unroll 1
   for (uint32_t c0 = 1; c0 <= B; c0 += 32) {
     uint32_t b = c0 + lane;
     uint32_t sz = b <= B ? smem[cnt + b] : 0u;
     if (sz > 0) {
       uint64_t key = (uint64_t)sz * (B + 1) + (tie_desc ? b : B - b);
       uint32_t rank = 0;
+#pragma unroll 1
       for (uint32_t b2 = 1; b2 <= B; ++b2) {
         uint32_t s2 = smem[cnt + b2];
         uint64_t k2 = (uint64_t)s2 * (B + 1) + (tie_desc ? b2 : B - b2);
@@ -179,9 +188,11 @@ __device__ PHB_COLD int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t
                                           int64_t dmax, const uint64_t* kl, uint64_t g,
                                           uint32_t m, int lane) {
   const uint32_t nwd = (uint32_t)((dmax + 32) >> 5);  // words of the valid mask
+#pragma unroll 1
   for (uint32_t g0 = 0; g0 < nwd; g0 += 96) {
     const uint32_t wb = g0 + 3u * lane;
     uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll 1
     for (uint32_t i = 0; i < k; ++i) {
       const uint32_t p = k <= (uint32_t)PMAX ? (uint32_t)pos16[i] : position(kl[i], g, m);
       const uint32_t W = occ + (p >> 5) + wb;
@@ -230,6 +241,7 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
   const uint64_t key0 = (uint32_t)lane < k ? kl[lane] : 0ull;
   const uint32_t scr_used = m / 32 + 2;
   uint32_t p0 = 0;  // this lane's base position (k <= 32)
+#pragma unroll 1
   for (int64_t s = s_begin;; ++s) {
     const int64_t pbase = s * (int64_t)m;
     if (s > 0 && pbase > cap) return {0, trials, 2};  // _kernels.py:324-328
@@ -242,6 +254,7 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
       coll = __any_sync(FULL, (uint32_t)lane < k && __popc(peers) > 1);
       if (!coll && (uint32_t)lane < k) pos16[lane] = (uint16_t)p0;
     } else {
+#pragma unroll 1
       for (uint32_t r = 0; r < R; ++r) {
         const uint32_t i = 32u * r + lane;
         bool c = false;
@@ -258,6 +271,7 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
         }
       }
       __syncwarp();
+#pragma unroll 1
       for (uint32_t w = lane; w < scr_used; w += 32) smem[scr + w] = 0;
     }
     __syncwarp();
@@ -272,19 +286,23 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
         } else if (R <= 32) {
           // a duplicate pair's later key found its slot taken: compare every
           // key that collided against the whole bucket
+#pragma unroll 1
           for (uint32_t r = 0; r < R; ++r) {
             uint32_t bal = __ballot_sync(FULL, (cmask >> r) & 1u);
             while (bal) {
               const uint32_t src = 32u * r + (__ffs(bal) - 1);
               bal &= bal - 1;
               const uint64_t v = kl[src];
+#pragma unroll 1
               for (uint32_t i2 = lane; i2 < k; i2 += 32)
                 if (i2 != src && kl[i2] == v) dup = true;
             }
           }
         } else {
+#pragma unroll 1
           for (uint32_t i = 0; i < k; ++i) {
             const uint64_t v = kl[i];
+#pragma unroll 1
             for (uint32_t i2 = lane; i2 < k; i2 += 32)
               if (i2 != i && kl[i2] == v) dup = true;
           }
@@ -302,6 +320,7 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
     const int64_t d = find_d(occ, pos16, k, dmax, kl, g, m, lane);
     if (d >= 0) {
       trials += (int64_t)k * (d + 1);
+#pragma unroll 1
       for (uint32_t i = lane; i < k; i += 32) {
         const uint32_t p =
             k <= 32 ? p0 : (i < (uint32_t)PMAX ? (uint32_t)pos16[i] : position(kl[i], g, m));
@@ -312,32 +331,6 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
       return {pbase + d, trials, 0};
     }
     trials += (int64_t)k * (dmax + 1);
-  }
-}
-
-// acc[t] |= window of 32 occupancy bits starting at bit 32*(R+t) + sh of w.
-// The ALU pipe (SHF, LOP3) is the binding unit of the search, so two of
-// every three windows are formed on the FMA pipe instead: with
-// P = 2^(32 - sh), (x >> sh) | (y << (32 - sh)) == hi(x * P) + lo(y * P).
-template <int R, int WPL>
-__device__ __forceinline__ void accumulate(uint32_t (&acc)[WPL], const uint32_t (&w)[16],
-                                           uint32_t sh) {
-  if (sh == 0) {
-#pragma unroll
-    for (int t = 0; t < WPL; ++t) acc[t] |= w[R + t];
-    return;
-  }
-  const uint32_t P = 1u << (32 - sh);
-#pragma unroll
-  for (int t = 0; t < WPL; ++t) {
-    uint32_t win;
-    if (!PHB_IMADFUN || t % 3 == 0) {
-      win = __funnelshift_r(w[R + t], w[R + t + 1], sh);
-    } else {
-      const uint32_t h = __umulhi(w[R + t], P);
-      win = w[R + t + 1] * P + h;
-    }
-    acc[t] |= win;
   }
 }
 
@@ -354,42 +347,33 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
                                      int64_t& s_next, int64_t trials, int max_batches,
                                      int lane) {
   constexpr int L = 32 / G, WPL = 96 / L;
+  constexpr uint32_t LMASK = L == 32 ? FULL : ((1u << L) - 1u);
   const int grp = lane / L, gl = lane % L;
   const bool act = (uint32_t)gl < k;
   const uint64_t key = act ? kl[gl] : 0ull;
-  const uint32_t gmask = L == 32 ? FULL : (((1u << L) - 1u) << (grp * L));
   uint16_t* const mypos = pos16 + grp * L;
+  const uint32_t wb = (uint32_t)gl * WPL;
+  // seeds s <= s_full sweep every displacement (dmax = m - 1, below the cap)
+  const int64_t s_full = cap >= (int64_t)m - 1 ? (cap - (int64_t)m + 1) / (int64_t)m : -1;
+#pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
     const int64_t s = s_next + grp;
-    const int64_t pbase = s * (int64_t)m;
     const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
     const uint32_t p = position(key, g, m);
     const uint32_t tag = act ? (((uint32_t)grp << 16) | p) : (0x80000000u | (uint32_t)lane);
     // every lane must execute the vote (no short-circuit around it)
     const uint32_t tpeers = __match_any_sync(FULL, tag);
-    const bool mycoll = act && __popc(tpeers) > 1;
-    const uint32_t cball = __ballot_sync(FULL, mycoll);
-#ifdef PHB_DEBUG
-    {
-      bool bf = false;
-      for (int o = 0; o < 32; ++o) {
-        uint32_t t2 = __shfl_sync(FULL, tag, o);
-        if (o != lane && t2 == tag && act) bf = true;
-      }
-      if (bf != mycoll) printf("match_any mismatch lane %d tag %x k %u G %d\n", lane, tag, k, G);
-    }
-#endif
+    const uint32_t cball = __ballot_sync(FULL, act && __popc(tpeers) > 1);
     if (act) mypos[gl] = (uint16_t)p;
     __syncwarp();
-    const bool gcoll = (cball & gmask) != 0;
-    const bool gcap = pbase > cap;
+    const bool gcoll = ((cball >> (grp * L)) & LMASK) != 0;
+    const int64_t pbase = s * (int64_t)m;
     int64_t dmax = cap - pbase;
     if (dmax > (int64_t)m - 1) dmax = (int64_t)m - 1;
-    uint32_t acc[WPL];
-    const bool dead_group = gcoll || gcap;
-    const uint32_t wb = (uint32_t)gl * WPL;
+    const bool dead_group = gcoll || pbase > cap;
     // start from "displacements past dmax are occupied": the partition's
     // mask table (dmax = m - 1) or, near the seed cap, computed here
+    uint32_t acc[WPL];
     if (PHB_MASKTAB && dmax == (int64_t)m - 1) {
 #pragma unroll
       for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : smem[dmask + wb + t];
@@ -401,36 +385,42 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         acc[t] = (dead_group || lt < 0) ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
       }
     }
+#if PHB_PAIR
+    // keys two at a time (an odd k repeats its last key; OR is idempotent),
+    // folding both windows with one 3-input OR
+#pragma unroll 1
+    for (uint32_t i = 0; i < k; i += 2) {
+      const uint32_t pa = mypos[i];
+      const uint32_t pb = mypos[i + 1 < k ? i + 1 : i];
+      const uint32_t sha = pa & 31, shb = pb & 31;
+      const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
+      uint32_t xa = smem[Wa], xb = smem[Wb];
+#pragma unroll
+      for (int t = 0; t < WPL; ++t) {
+        const uint32_t ya = smem[Wa + t + 1], yb = smem[Wb + t + 1];
+        acc[t] |= __funnelshift_r(xa, ya, sha) | __funnelshift_r(xb, yb, shb);
+        xa = ya;
+        xb = yb;
+      }
+      if ((i & 2) == 2) {  // every 4 keys: stop once no displacement can survive
+        uint32_t all = FULL;
+#pragma unroll
+        for (int t = 0; t < WPL; ++t) all &= acc[t];
+        if (__all_sync(FULL, all == FULL)) break;
+      }
+    }
+#else
+#pragma unroll 1
     for (uint32_t i = 0; i < k; ++i) {
       const uint32_t pi = mypos[i];
       const uint32_t sh = pi & 31;
-      if constexpr (G == 4 && PHB_LDS128) {
-        // 8 lanes x 12 words: 16-byte aligned LDS.128 reads cover each lane's
-        // 13 words in 4 loads, conflict-free per quarter-warp (lanes 12*gl
-        // words apart tile all 32 banks); the word offset r = (p >> 5) & 3
-        // is warp-uniform, so the funnel shifts use static register indices.
-        const uint32_t A = occ + ((pi >> 5) & ~3u) + wb;
-        uint32_t w[16];
+      const uint32_t W = occ + (pi >> 5) + wb;
+      uint32_t x = smem[W];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 q = *reinterpret_cast<const uint4*>(&smem[A + 4 * c]);
-          w[4 * c] = q.x, w[4 * c + 1] = q.y, w[4 * c + 2] = q.z, w[4 * c + 3] = q.w;
-        }
-        switch ((pi >> 5) & 3u) {
-          case 0: accumulate<0, WPL>(acc, w, sh); break;
-          case 1: accumulate<1, WPL>(acc, w, sh); break;
-          case 2: accumulate<2, WPL>(acc, w, sh); break;
-          default: accumulate<3, WPL>(acc, w, sh); break;
-        }
-      } else {
-        const uint32_t W = occ + (pi >> 5) + wb;
-        uint32_t x = smem[W];
-#pragma unroll
-        for (int t = 0; t < WPL; ++t) {
-          const uint32_t y = smem[W + t + 1];
-          acc[t] |= __funnelshift_r(x, y, sh);
-          x = y;
-        }
+      for (int t = 0; t < WPL; ++t) {
+        const uint32_t y = smem[W + t + 1];
+        acc[t] |= __funnelshift_r(x, y, sh);
+        x = y;
       }
       if ((i & 3) == 3) {
         uint32_t all = FULL;
@@ -439,6 +429,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         if (__all_sync(FULL, all == FULL)) break;
       }
     }
+#endif
     // this lane's first valid displacement (d <= dmax), or -1
     uint32_t sat = FULL;
 #pragma unroll
@@ -451,11 +442,40 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
       for (int t = WPL - 1; t >= 0; --t)
         if (acc[t] != FULL) myd = 32 * (int64_t)(wb + t) + (__ffs(~acc[t]) - 1);
     }
-    // resolve the G seeds in order, like the sequential loop
+    if (PHB_FASTRES && s_next > 0 && s_next + G - 1 <= s_full) {
+      // common case: no seed of the batch touches the cap or s = 0. The
+      // sequential loop's outcome in closed form: seeds before the first
+      // group with a valid displacement either self-collided (k trials) or
+      // swept all m displacements (k*m trials).
+      uint32_t collm = 0, foundm = 0;
+#pragma unroll
+      for (int gi = 0; gi < G; ++gi) {
+        collm |= (uint32_t)(((cball >> (gi * L)) & LMASK) != 0) << gi;
+        foundm |= (uint32_t)(((fball >> (gi * L)) & LMASK) != 0) << gi;
+      }
+      const int gw = foundm ? __ffs(foundm) - 1 : G;
+      const int ncoll = __popc(collm & ((1u << gw) - 1u));
+      trials += (int64_t)k * ncoll + (int64_t)k * m * (gw - ncoll);
+      if (foundm) {
+        const int64_t d = __shfl_sync(FULL, myd, __ffs((fball >> (gw * L)) & LMASK) - 1 + gw * L);
+        trials += (int64_t)k * (d + 1);
+        if (grp == gw && act) {
+          uint32_t slot = p + (uint32_t)d;
+          if (slot >= m) slot -= m;
+          mark(occ, slot, m, 100 * G + (int)k);
+        }
+        return {(s_next + gw) * (int64_t)m + d, trials, 0};
+      }
+      s_next += G;
+      __syncwarp();
+      continue;
+    }
+    // general resolution (s = 0 duplicate check, seed cap): seed by seed
+#pragma unroll 1
     for (int gi = 0; gi < G; ++gi) {
       const int64_t si = s_next + gi;
       const int64_t pb = si * (int64_t)m;
-      const uint32_t gm = L == 32 ? FULL : (((1u << L) - 1u) << (gi * L));
+      const uint32_t gm = LMASK << (gi * L);
       const bool ci = (cball & gm) != 0;
       if (si > 0 && pb > cap) return {0, trials, 2};
       if (si == 0) {
@@ -508,6 +528,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
   const uint64_t g0 = mix64(POSITION_SALT);  // s = 0
   const int64_t cap = a.seed_cap;
 
+#pragma unroll 1
   for (;;) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(a.queue, 1u);
@@ -526,11 +547,14 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
     }
 
     // ---- bucket histogram + counting sort into glo (_kernels.py:252-266)
+#pragma unroll 1
     for (uint32_t b = lane; b <= B; b += 32) smem[cnt + b] = 0;
     __syncwarp();
+#pragma unroll 1
     for (uint32_t q = lane; q < m; q += 32) atomicAdd(&smem[cnt + a.bid[kb + q]], 1u);
     __syncwarp();
     uint32_t run = 0, maxsz = 0;
+#pragma unroll 1
     for (uint32_t c0 = 1; c0 <= B; c0 += 32) {
       uint32_t b = c0 + lane;
       uint32_t v = b <= B ? smem[cnt + b] : 0u;
@@ -541,15 +565,19 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
     }
     maxsz = warp_max(maxsz);
     __syncwarp();
+#pragma unroll 1
     for (uint32_t q = lane; q < m; q += 32) {
       const uint32_t b = a.bid[kb + q];
       const uint32_t at = atomicAdd(&smem[endp + b], 1u);
       a.glo[kb + at] = a.lo[kb + q];
     }
     const uint32_t occ_used = min((uint32_t)plan.occ_w, (2 * m) / 32 + 104);
+#pragma unroll 1
     for (uint32_t w = lane; w < occ_used; w += 32) smem[occ + w] = 0;
     const uint32_t scr_used = m / 32 + 2;
+#pragma unroll 1
     for (uint32_t w = lane; w < scr_used; w += 32) smem[scr + w] = 0;
+#pragma unroll 1
     for (uint32_t w = lane; w < 96; w += 32) {
       const int64_t lt = (int64_t)m - 1 - 32 * (int64_t)w;  // last valid bit of word w
       smem[dmask + w] = lt < 0 ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
@@ -563,6 +591,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
     int64_t ptrials = 0;
     uint8_t status = 0;
     const bool small_ok = m <= 3072;
+#pragma unroll 1
     for (uint32_t oi = 0; oi < nb; ++oi) {
       const uint32_t b = order[oi];
       const uint32_t k = smem[cnt + b];

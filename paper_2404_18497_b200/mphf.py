@@ -128,7 +128,7 @@ class BuildEngine:
         self._pinned.copy_(stats, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        counts.zero_()  # reused as the scatter cursors
+        # counts is reused as the scatter cursors (phb_scatter initialises them)
         lo = torch.empty(n, dtype=torch.int64, device=dev)
         bid = torch.empty(n, dtype=torch.int16, device=dev)
         _native.check(L.phb_scatter(buf, offs, k64, n, seed, nparts, P(self.entries), B,
