@@ -188,3 +188,57 @@ def test_strings_vs_oracle(phb, orc):
     ref = orc.build((buf, off), lambda_=8.0, P=2500.0, encoder="ic-r")
     assert f.serialize() == ref.serialize()
     assert f.is_bijection_on(corpus)
+
+
+@pytest.mark.parametrize("lam,P,n,enc", [
+    (10.0, 6000.0, 60_000, "ic-r"),    # m ~ 6000 > 3072: generic search path, multi-pass windows
+    (11.0, 12000.0, 48_000, "ic-c"),   # very large partitions, buckets > 256 keys
+    (1.0, 300.0, 60_000, "mono-c"),    # B = P: many empty / singleton buckets
+    (3.0, 40.0, 50_000, "mixed:3"),    # tiny partitions
+])
+def test_unusual_configs_vs_oracle(phb, orc, lam, P, n, enc):
+    from paper_2404_18497_b200.keygen import synth_u64
+
+    keys = synth_u64(n, int(lam * 1000 + P))
+    cfg = phb.BuildConfig(lambda_=lam, partition_size=P, encoder=enc)
+    f = phb.build(keys, cfg)
+    ref = orc.build(keys, lambda_=lam, P=P, encoder=enc)
+    assert f.serialize() == ref.serialize()
+    assert f.stats.trials_total == int(ref.trials.sum())
+    assert f.is_bijection_on(keys)
+
+
+def test_strings_million_vs_oracle(phb, orc):
+    rng = np.random.default_rng(12)
+    n = 1_000_000
+    lens = rng.integers(10, 101, size=n)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    buf = rng.integers(33, 127, size=int(off[-1]), dtype=np.uint8)
+    corpus = phb.KeyCorpus(buf, off)
+    for enc in ("ic-r", "mono-r"):
+        f = phb.build(corpus, phb.BuildConfig(lambda_=8.0, partition_size=2500.0, encoder=enc))
+        ref = orc.build((buf, off), lambda_=8.0, P=2500.0, encoder=enc)
+        assert f.serialize() == ref.serialize()
+    q = f.query_many(corpus)
+    hi, lo = orc.murmur3_many(buf, off, f.global_seed)
+    assert np.array_equal(q, ref.query_hashes(hi, lo))
+
+
+@pytest.mark.slow
+def test_hundred_million_properties(phb):
+    """Full C2 size: bijection, determinism and input-order independence."""
+    from paper_2404_18497_b200.keygen import synth_u64_device
+
+    n = 100_000_000
+    keys = synth_u64_device(n, 0)
+    cfg = phb.BuildConfig(lambda_=9.0, partition_size=2500.0, encoder="ic-c")
+    f = phb.build(keys, cfg)
+    assert f.is_bijection_on(keys)
+    assert 2.10 < f.bits_per_key() < 2.20
+    perm = torch.randperm(n, device=keys.device)
+    g = phb.build(keys[perm], cfg)
+    assert f._body.tobytes() == g._body.tobytes()
+    h = phb.Mphf.deserialize(f.serialize())
+    sample = keys[:5_000_000]
+    assert torch.equal(h.query_device(sample), f.query_device(sample))
