@@ -110,7 +110,7 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_init(n_gpus: int):
+def dist_init(n_gpus: int, backend: str = "nccl", same_device: bool = False):
     import torch
 
     rank = int(os.environ.get("RANK", "0"))
@@ -119,8 +119,13 @@ def dist_init(n_gpus: int):
     if world > 1:
         import torch.distributed as dist
 
+        if same_device:  # validation mode: every rank on GPU 0 (gloo carries CUDA tensors)
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -193,7 +198,7 @@ def run_gpu(args):
     from paper_2404_18497_b200.keygen import synth_u64_device, to_device
     from paper_2404_18497_b200.mphf import BuildEngine
 
-    rank, world, local = dist_init(args.gpus)
+    rank, world, local = dist_init(args.gpus, args.backend, args.same_device)
     dev = torch.device("cuda", torch.cuda.current_device())
     n = args.n
     cfg = phb.BuildConfig(lambda_=LAMBDA, partition_size=PSIZE, encoder=ENCODER)
@@ -371,10 +376,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_KEYS)
+    ap.add_argument("--keys", dest="n", type=int, default=N_KEYS, help="keys per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", help="nccl (default) or gloo (validation)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="validation: run every rank on GPU 0 (with --backend gloo)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

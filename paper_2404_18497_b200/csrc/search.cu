@@ -40,6 +40,12 @@ namespace phb {
 #ifndef PHB_MASKTAB
 #define PHB_MASKTAB 1
 #endif
+#ifndef PHB_LDS64
+#define PHB_LDS64 0  // measured slower (round 1)
+#endif
+#ifndef PHB_PREFETCH
+#define PHB_PREFETCH 1
+#endif
 #ifndef PHB_PAIR
 #define PHB_PAIR 0  // measured slower (round 1)
 #endif
@@ -410,17 +416,47 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
       }
     }
 #else
+    // the next key's base position is loaded one iteration ahead, so its
+    // shared-memory latency hides behind the current key's window loads
+    uint32_t pnext = mypos[0];
 #pragma unroll 1
     for (uint32_t i = 0; i < k; ++i) {
-      const uint32_t pi = mypos[i];
+      const uint32_t pi = pnext;
+      if (PHB_PREFETCH) pnext = mypos[i + 1 < k ? i + 1 : i];
+      else if (i + 1 < k) pnext = mypos[i + 1];
       const uint32_t sh = pi & 31;
       const uint32_t W = occ + (pi >> 5) + wb;
-      uint32_t x = smem[W];
+      if constexpr (PHB_LDS64 && (WPL % 2) == 0) {
+        // wb is even for G = 4 / 2, so the word parity of W is warp-uniform:
+        // read the lane's WPL + 1 words with 64-bit loads (one 32-bit load
+        // first when W is odd), then the same funnel-shift block
+        uint32_t w[WPL + 2];
+        if (W & 1u) {
+          w[0] = smem[W];
 #pragma unroll
-      for (int t = 0; t < WPL; ++t) {
-        const uint32_t y = smem[W + t + 1];
-        acc[t] |= __funnelshift_r(x, y, sh);
-        x = y;
+          for (int c = 0; c < WPL / 2; ++c) {
+            const uint2 v = *reinterpret_cast<const uint2*>(&smem[W + 1 + 2 * c]);
+            w[1 + 2 * c] = v.x;
+            w[2 + 2 * c] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c <= WPL / 2; ++c) {
+            const uint2 v = *reinterpret_cast<const uint2*>(&smem[W + 2 * c]);
+            w[2 * c] = v.x;
+            w[2 * c + 1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < WPL; ++t) acc[t] |= __funnelshift_r(w[t], w[t + 1], sh);
+      } else {
+        uint32_t x = smem[W];
+#pragma unroll
+        for (int t = 0; t < WPL; ++t) {
+          const uint32_t y = smem[W + t + 1];
+          acc[t] |= __funnelshift_r(x, y, sh);
+          x = y;
+        }
       }
       if ((i & 3) == 3) {
         uint32_t all = FULL;

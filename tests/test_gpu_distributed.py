@@ -66,3 +66,48 @@ def test_nccl_world1_equals_single_gpu_build():
     assert f.serialize() == g.serialize()
     assert f.stats.trials_total == g.stats.trials_total
     assert f.is_bijection_on(keys)
+
+
+def _dev_worker(rank, world, path, keys, cfg_kw, out_path):
+    import torch.distributed as dist
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.distributed import build_distributed
+
+    torch.cuda.set_device(0)  # every rank shares the one GPU; gloo carries CUDA tensors
+    dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
+    try:
+        shards = np.array_split(keys, world)
+        f = build_distributed(shards[rank], phb.BuildConfig(**cfg_kw))
+        out = f.query_device(shards[rank])
+        ok = bool(((out >= 0) & (out < f.n)).all()) and out.unique().numel() == out.numel()
+        outs = [torch.empty(len(s), dtype=torch.int64, device="cuda") for s in shards]
+        dist.all_gather(outs, out)
+        allout = torch.cat(outs)
+        ok = ok and allout.unique().numel() == f.n
+        np.save(out_path + f".{rank}.npy", np.frombuffer(f.serialize(), np.uint8))
+        np.save(out_path + f".{rank}.ok.npy", np.array([ok, f.stats.trials_total]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_sharded_build_gloo_on_one_gpu(world):
+    """The DeviceOps path (K1/K3 per shard, all-to-all, phb_regroup, K4 on
+    owned partitions, seed all_gather, K5) with `world` ranks sharing one
+    GPU over gloo: every rank's bytes equal the single-GPU build."""
+    import torch.multiprocessing as mp
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.keygen import synth_u64
+
+    keys = synth_u64(300_000, 11)
+    cfg_kw = dict(lambda_=7.0, partition_size=2500.0, encoder="ic-r")
+    d = tempfile.mkdtemp()
+    out = os.path.join(d, "blob")
+    mp.spawn(_dev_worker, args=(world, os.path.join(d, "rdv"), keys, cfg_kw, out), nprocs=world)
+    want = phb.build(keys, phb.BuildConfig(**cfg_kw))
+    for r in range(world):
+        assert np.load(out + f".{r}.npy").tobytes() == want.serialize()
+        ok, trials = np.load(out + f".{r}.ok.npy")
+        assert ok and trials == want.stats.trials_total
