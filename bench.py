@@ -233,7 +233,7 @@ def run_gpu(args):
         dops = DeviceOps(cfg)
 
         def step():
-            return build_distributed(dk, cfg, ops=dops, to_host=False)
+            return build_distributed(dk, cfg, ops=dops, to_host=False, transport=args.transport)
     else:
         def step():
             return eng.run(dk, 0)
@@ -279,7 +279,7 @@ def run_gpu(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         if world > 1:
-            f = build_distributed(host, cfg, ops=dops)
+            f = build_distributed(host, cfg, ops=dops, transport=args.transport)
         else:
             f = phb.build(host, cfg)
         e1.record()
@@ -291,7 +291,8 @@ def run_gpu(args):
     e2e = allmax(statistics.median(e2e_ms) if e2e_ms else float("nan"), world)
 
     # ---- batched GPU query of all n keys (Mq/s), from the last build
-    f = build_distributed(host, cfg, ops=dops) if world > 1 else phb.build(host, cfg)
+    f = (build_distributed(host, cfg, ops=dops, transport=args.transport) if world > 1
+         else phb.build(host, cfg))
     qkeys = host.to(dev)
     qdk = to_device(qkeys, dev)
     out = f.query_device(qdk)
@@ -338,8 +339,8 @@ def run_gpu(args):
                    "encoder": ENCODER, "global_seed": 0,
                    "l2": "inputs (800 MB keys + 1 GB grouped records) exceed the 126 MB L2",
                    "keys": "mix64(rank*n + i), distinct by construction",
-                   "parallelism": (f"sharded build x{world}: NCCL all-to-all routing of "
-                                   "records to partition owners" if world > 1 else "1 GPU")},
+                   "parallelism": (f"sharded build x{world}: records routed to partition "
+                                   f"owners ({args.transport})" if world > 1 else "1 GPU")},
         "ns_per_key": ms * 1e6 / total_keys,
         "bits_per_key": bits,
         "query": {"value": total_keys / (allmax(q_ms, world) * 1e-3) / 1e6, "unit": "Mq/s",
@@ -381,6 +382,9 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--backend", default="nccl", help="nccl (default) or gloo (validation)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 record routing: fused CUDA-IPC peer scatter (default) or NCCL "
+                         "all-to-all + regroup (automatic fallback if peer mapping fails)")
     ap.add_argument("--same-device", action="store_true",
                     help="validation: run every rank on GPU 0 (with --backend gloo)")
     args = ap.parse_args()

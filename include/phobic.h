@@ -172,6 +172,28 @@ int phb_offsets_from_deltas(const int64_t* deltas, int64_t n, int64_t nparts, in
 int phb_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t* counts, int64_t G,
                 int64_t np, uint64_t* lo_out, uint16_t* aux_out, int64_t* key_off, void* stream);
 
+/* Fused multi-GPU route (distributed.py, transport="p2p"): K3 scatter and the
+ * all-to-all in one kernel. Each local key's (lo, bucket id) is stored
+ * directly into its owner rank's receive buffer over NVLink peer memory, at
+ * part_base[j] + (rank of the key among this source's keys of partition j).
+ * part_base: device i64[nparts]; owner: device u8[nparts] (owner rank of
+ * partition j); lo_dst / bid_dst: HOST arrays of G device pointers (peer
+ * buffers mapped with phb_ipc_open, the local one for g == rank); cursor:
+ * device u32[nparts] scratch. The caller orders the kernel before the
+ * owners' reads (stream sync + group barrier). */
+int phb_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
+                    uint64_t seed, int64_t nparts, const double* entries, int32_t bcount,
+                    const int64_t* part_base, const uint8_t* owner, uint64_t* const* lo_dst,
+                    uint16_t* const* bid_dst, int32_t G, uint32_t* cursor, void* stream);
+
+/* CUDA IPC plumbing for the peer buffers (64-byte cudaIpcMemHandle_t). */
+int phb_ipc_alloc(size_t bytes, void** dptr);
+int phb_ipc_free(void* dptr);
+int phb_ipc_handle(void* dptr, uint8_t* handle64);
+int phb_ipc_open(const uint8_t* handle64, void** dptr);
+int phb_ipc_close(void* dptr);
+int phb_sync(void* stream);
+
 /* Synthetic distinct 64-bit keys for benchmarks: out[i] = mix64(offset + i)
  * (mix64 is a bijection on u64, so keys are distinct for distinct i). The
  * host restatement is keygen.synth_u64. Not a reference interface: bench

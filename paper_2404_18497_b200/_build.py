@@ -19,7 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = os.environ.get("PHB_NVCC_EXTRA", "").split() + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-O3",
          "--expt-relaxed-constexpr"]
-SOURCES = ["hash.cu", "layout.cu", "search.cu", "encode.cu", "decode.cu", "query.cu", "capi.cu"]
+SOURCES = ["hash.cu", "layout.cu", "search.cu", "encode.cu", "decode.cu", "query.cu", "p2p.cu",
+           "capi.cu"]
 
 
 def _stale(target: Path, deps) -> bool:

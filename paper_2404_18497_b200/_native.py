@@ -43,6 +43,13 @@ SIGNATURES = {
     "phb_device_sms": [],
     "phb_synth_keys": [P, I64, U64, P],
     "phb_regroup": [P, P, P, I64, I64, P, P, P, P],
+    "phb_scatter_p2p": [P, P, P, I64, U64, I64, P, I32, P, P, P, P, I32, P, P],
+    "phb_ipc_alloc": [SZ, P],
+    "phb_ipc_free": [P],
+    "phb_ipc_handle": [P, P],
+    "phb_ipc_open": [P, P],
+    "phb_ipc_close": [P],
+    "phb_sync": [P],
 }
 OTHER = {
     "phb_version": ([], ctypes.c_char_p),

@@ -104,7 +104,7 @@ def _dev_u64(a, dev) -> torch.Tensor:
 
 
 def device_table(table: AssignmentTable, dev) -> torch.Tensor:
-    return torch.from_numpy(np.ascontiguousarray(table.entries, dtype=np.float64)).to(dev)
+    return torch.from_numpy(np.array(table.entries, dtype=np.float64)).to(dev)
 
 
 def build_partition_range(his, los, key_offsets, p_lo: int, p_hi: int, table: AssignmentTable,

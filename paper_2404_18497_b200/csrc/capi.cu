@@ -2,6 +2,7 @@
 // Thin argument marshalling around the launchers; no state survives a call.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "../../include/phobic.h"
 #include "common.cuh"
@@ -309,6 +310,41 @@ int phb_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t* co
                 int64_t np, uint64_t* lo_out, uint16_t* aux_out, int64_t* key_off, void* stream) {
   return launch_regroup(lo_in, aux_in, counts, G, np, lo_out, aux_out, key_off, S(stream));
 }
+
+int phb_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
+                    uint64_t seed, int64_t nparts, const double* entries, int32_t bcount,
+                    const int64_t* part_base, const uint8_t* owner, uint64_t* const* lo_dst,
+                    uint16_t* const* bid_dst, int32_t G, uint32_t* cursor, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (!lo_dst || !bid_dst) return PHB_E_ARGS;
+  return launch_scatter_p2p(buf, offsets, keys64, n, seed, nparts, entries, (uint32_t)bcount,
+                            part_base, owner, lo_dst, bid_dst, G, cursor, S(stream));
+}
+
+int phb_ipc_alloc(size_t bytes, void** dptr) {
+  if (!dptr) return PHB_E_ARGS;
+  return (int)cudaMalloc(dptr, bytes ? bytes : 16);
+}
+
+int phb_ipc_free(void* dptr) { return (int)cudaFree(dptr); }
+
+int phb_ipc_handle(void* dptr, uint8_t* handle64) {
+  cudaIpcMemHandle_t h;
+  PHB_CUDA_TRY(cudaIpcGetMemHandle(&h, dptr));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, 64);
+  return 0;
+}
+
+int phb_ipc_open(const uint8_t* handle64, void** dptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  return (int)cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+}
+
+int phb_ipc_close(void* dptr) { return (int)cudaIpcCloseMemHandle(dptr); }
+
+int phb_sync(void* stream) { return (int)cudaStreamSynchronize(S(stream)); }
 
 int phb_synth_keys(uint64_t* out, int64_t n, uint64_t offset, void* stream) {
   if (n < 0) return PHB_E_ARGS;

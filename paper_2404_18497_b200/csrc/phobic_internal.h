@@ -34,6 +34,12 @@ int launch_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t*
                    int64_t np, uint64_t* lo_out, uint16_t* aux_out, int64_t* key_off,
                    cudaStream_t st);
 
+int launch_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
+                       int64_t n, uint64_t seed, int64_t nparts, const double* entries,
+                       uint32_t bcount, const int64_t* part_base, const uint8_t* owner,
+                       uint64_t* const* lo_dst, uint16_t* const* bid_dst, int32_t G,
+                       uint32_t* cursor, cudaStream_t st);
+
 // search.cu
 struct SearchArgs {
   const uint64_t* lo;

@@ -148,10 +148,15 @@ def _as_bytes(t: torch.Tensor) -> torch.Tensor:
 
 
 def build_distributed(local_keys, config: BuildConfig | None = None, group=None, ops=None,
-                      to_host: bool = True):
+                      to_host: bool = True, transport: str = "nccl"):
     """Collective build: every rank passes its shard; every rank returns the
     same Mphf (global n, identical bytes for any world size). With
-    to_host=False the device-resident DeviceBuild is returned instead."""
+    to_host=False the device-resident DeviceBuild is returned instead.
+
+    transport: "nccl" = K3 + all_to_all_single + phb_regroup; "p2p" = the
+    fused route, K3 writing every record straight into its owner's buffer
+    over CUDA-IPC peer memory (phb_scatter_p2p; one process per GPU on one
+    node)."""
     from .mphf import BuildStats, DeviceBuild, DuplicateKeys, Mphf
 
     config = config or BuildConfig()
@@ -180,25 +185,35 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
         C = torch.stack(gathered).to(torch.int64)            # [G, nparts]
         total_counts = C.sum(0).to(torch.int32)
         key_off_g, deltas, stats = ops.layout(total_counts, n, nparts)
-        # 3. group own keys by partition (hence by destination rank)
-        key_off_l = torch.zeros(nparts + 1, dtype=torch.int64, device=C.device)
-        torch.cumsum(C[rank], 0, out=key_off_l[1:])
-        lo, aux = ops.scatter(dk, seed, nparts, key_off_l)
-        kb = key_off_l[torch.tensor(bounds, device=C.device)].cpu().tolist()
-        send = [kb[g + 1] - kb[g] for g in range(world)]
         C_owned = C[:, p_lo:p_hi]
-        recv = C_owned.sum(1).cpu().tolist()
-        # 4. all-to-all of the records (byte views: gloo/NCCL-safe dtypes)
-        esz = aux.element_size()
-        lo_r = torch.empty(sum(recv), dtype=lo.dtype, device=lo.device)
-        aux_r = torch.empty(sum(recv) * esz, dtype=torch.uint8, device=lo.device)
-        dist.all_to_all_single(lo_r, lo, recv, send, group=group)
-        dist.all_to_all_single(aux_r, _as_bytes(aux), [r * esz for r in recv],
-                               [s * esz for s in send], group=group)
-        aux_r = aux_r.view(aux.dtype)
-        # 5. merge the G partition-sorted chunks
-        lo_g, aux_g, key_off_own = ops.regroup(lo_r, aux_r, C_owned, recv)
         m_max = int(C_owned.sum(0).max().item()) if np_g else 0
+        routed = None
+        if transport == "p2p":
+            # 3-5 fused: records land partition-grouped in the owner's buffer
+            routed = _route_p2p(ops, dk, seed, nparts, C, bounds, rank, world, group)
+            if routed is None:  # peer mapping unavailable on some rank: collective fallback
+                transport = "nccl"
+        if routed is not None:
+            lo_g, aux_g, key_off_own, route = routed
+        else:
+            # 3. group own keys by partition (hence by destination rank)
+            key_off_l = torch.zeros(nparts + 1, dtype=torch.int64, device=C.device)
+            torch.cumsum(C[rank], 0, out=key_off_l[1:])
+            lo, aux = ops.scatter(dk, seed, nparts, key_off_l)
+            kb = key_off_l[torch.tensor(bounds, device=C.device)].cpu().tolist()
+            send = [kb[g + 1] - kb[g] for g in range(world)]
+            recv = C_owned.sum(1).cpu().tolist()
+            # 4. all-to-all of the records (byte views: gloo/NCCL-safe dtypes)
+            esz = aux.element_size()
+            lo_r = torch.empty(sum(recv), dtype=lo.dtype, device=lo.device)
+            aux_r = torch.empty(sum(recv) * esz, dtype=torch.uint8, device=lo.device)
+            dist.all_to_all_single(lo_r, lo, recv, send, group=group)
+            dist.all_to_all_single(aux_r, _as_bytes(aux), [r * esz for r in recv],
+                                   [s * esz for s in send], group=group)
+            aux_r = aux_r.view(aux.dtype)
+            # 5. merge the G partition-sorted chunks
+            lo_g, aux_g, key_off_own = ops.regroup(lo_r, aux_r, C_owned, recv)
+            route = None
         # 6. search + collective failure / trials
         if np_g:
             seeds_own, part_trials, status = ops.search(lo_g, aux_g, key_off_own, np_g, m_max)
@@ -210,6 +225,8 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
         else:
             seeds_own = torch.zeros((config.bucket_count, 0), dtype=torch.int64, device=C.device)
             bad, code, trials = nparts, 0, 0
+        if route is not None:  # every rank, even one without partitions (barrier inside)
+            route.release_after_search()
         flag = torch.tensor([bad, trials], dtype=torch.int64, device=C.device)
         red = flag.clone()
         dist.all_reduce(red[0:1], op=dist.ReduceOp.MIN, group=group)
@@ -244,6 +261,107 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
     raise DuplicateKeys(
         f"construction failed after {MAX_ATTEMPTS} seeds ({SeedExhausted(last)}); "
         "input most likely contains duplicate keys")
+
+
+class _Route:
+    """CUDA-IPC peer buffers of one p2p routing step."""
+
+    def __init__(self, lo_ptr, bid_ptr, n, peers, group):
+        self.lo_ptr, self.bid_ptr, self.n, self.peers, self.group = lo_ptr, bid_ptr, n, peers, group
+
+    def release_after_search(self):
+        L = _native.lib()
+        _native.check(L.phb_sync(_native.stream()), "phb_sync")
+        for p in self.peers:  # mapped peer buffers (not ours)
+            _native.check(L.phb_ipc_close(p), "phb_ipc_close")
+        dist.barrier(group=self.group)  # every peer unmapped our buffer
+        _native.check(L.phb_ipc_free(self.lo_ptr), "phb_ipc_free")
+        _native.check(L.phb_ipc_free(self.bid_ptr), "phb_ipc_free")
+        self.peers = []
+
+
+class _PtrTensor:
+    """Minimal tensor-like view of a raw device pointer for _native.ptr()."""
+
+    def __init__(self, ptr: int, n: int):
+        self._p, self._n = ptr, n
+
+    def data_ptr(self) -> int:
+        return self._p
+
+    def numel(self) -> int:
+        return self._n
+
+
+def _route_p2p(ops: DeviceOps, dk: DeviceKeys, seed: int, nparts: int, C: torch.Tensor,
+               bounds: list[int], rank: int, world: int, group):
+    """Fused K3 + all-to-all over peer memory (phb_scatter_p2p)."""
+    L = _native.lib()
+    dev = ops.dev
+    total = C.sum(0)                                       # [nparts] global counts
+    ex = torch.zeros(nparts + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(total.to(dev), 0, out=ex[1:])
+    owner = torch.empty(nparts, dtype=torch.uint8, device=dev)
+    start = torch.empty(nparts, dtype=torch.int64, device=dev)
+    for g in range(world):
+        owner[bounds[g]:bounds[g + 1]] = g
+        start[bounds[g]:bounds[g + 1]] = ex[bounds[g]]
+    before = (C[:rank].sum(0) if rank else torch.zeros_like(total)).to(dev)
+    part_base = (ex[:-1] - start + before).contiguous()   # my first slot per partition
+    p_lo, p_hi = bounds[rank], bounds[rank + 1]
+    recv_n = int((ex[p_hi] - ex[p_lo]).item())
+    # my receive buffers (IPC-able cudaMalloc) and the peers' handles
+    lo_p, bid_p = ctypes.c_void_p(), ctypes.c_void_p()
+    _native.check(L.phb_ipc_alloc(max(recv_n, 1) * 8, ctypes.byref(lo_p)), "phb_ipc_alloc")
+    _native.check(L.phb_ipc_alloc(max(recv_n, 1) * 2, ctypes.byref(bid_p)), "phb_ipc_alloc")
+    hbuf = np.zeros(128, np.uint8)
+    _native.check(L.phb_ipc_handle(lo_p, hbuf.ctypes.data_as(ctypes.c_void_p)), "phb_ipc_handle")
+    _native.check(L.phb_ipc_handle(bid_p, hbuf[64:].ctypes.data_as(ctypes.c_void_p)),
+                  "phb_ipc_handle")
+    comm_dev = C.device
+    mine = torch.from_numpy(hbuf).to(comm_dev)
+    allh = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allh, mine, group=group)
+    lo_ptrs = (ctypes.c_void_p * world)()
+    bid_ptrs = (ctypes.c_void_p * world)()
+    opened = []
+    ok = True
+    for g in range(world):
+        if g == rank:
+            lo_ptrs[g], bid_ptrs[g] = lo_p.value, bid_p.value
+            continue
+        h = np.ascontiguousarray(allh[g].cpu().numpy())
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        if L.phb_ipc_open(h.ctypes.data_as(ctypes.c_void_p), ctypes.byref(a)) != 0:
+            ok = False
+            break
+        opened.append(a.value)
+        if L.phb_ipc_open(h[64:].ctypes.data_as(ctypes.c_void_p), ctypes.byref(b)) != 0:
+            ok = False
+            break
+        opened.append(b.value)
+        lo_ptrs[g], bid_ptrs[g] = a.value, b.value
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=comm_dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:  # undo and let every rank take the NCCL route
+        for ptr in opened:
+            L.phb_ipc_close(ptr)
+        dist.barrier(group=group)
+        L.phb_ipc_free(lo_p)
+        L.phb_ipc_free(bid_p)
+        return None
+    cursor = torch.empty(nparts, dtype=torch.int32, device=dev)
+    P = _native.ptr
+    _native.check(L.phb_scatter_p2p(
+        None if dk.is_u64 else P(dk.buf), None if dk.is_u64 else P(dk.offsets),
+        P(dk.keys64) if dk.is_u64 else None, dk.n, seed, nparts, P(ops.entries), ops.B,
+        P(part_base), P(owner), lo_ptrs, bid_ptrs, world, P(cursor), _native.stream()),
+        "phb_scatter_p2p")
+    _native.check(L.phb_sync(_native.stream()), "phb_sync")
+    dist.barrier(group=group)  # every source finished writing into every owner
+    key_off_own = (ex[p_lo:p_hi + 1] - ex[p_lo]).contiguous()
+    route = _Route(lo_p.value, bid_p.value, recv_n, opened, group)
+    return (_PtrTensor(lo_p.value, recv_n), _PtrTensor(bid_p.value, recv_n), key_off_own, route)
 
 
 class _EngineView:

@@ -68,7 +68,7 @@ def test_nccl_world1_equals_single_gpu_build():
     assert f.is_bijection_on(keys)
 
 
-def _dev_worker(rank, world, path, keys, cfg_kw, out_path):
+def _dev_worker(rank, world, path, keys, cfg_kw, out_path, transport="nccl"):
     import torch.distributed as dist
 
     import paper_2404_18497_b200 as phb
@@ -78,7 +78,7 @@ def _dev_worker(rank, world, path, keys, cfg_kw, out_path):
     dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
     try:
         shards = np.array_split(keys, world)
-        f = build_distributed(shards[rank], phb.BuildConfig(**cfg_kw))
+        f = build_distributed(shards[rank], phb.BuildConfig(**cfg_kw), transport=transport)
         out = f.query_device(shards[rank])
         ok = bool(((out >= 0) & (out < f.n)).all()) and out.unique().numel() == out.numel()
         outs = [torch.empty(len(s), dtype=torch.int64, device="cuda") for s in shards]
@@ -91,11 +91,13 @@ def _dev_worker(rank, world, path, keys, cfg_kw, out_path):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_device_sharded_build_gloo_on_one_gpu(world):
-    """The DeviceOps path (K1/K3 per shard, all-to-all, phb_regroup, K4 on
-    owned partitions, seed all_gather, K5) with `world` ranks sharing one
-    GPU over gloo: every rank's bytes equal the single-GPU build."""
+def test_device_sharded_build_gloo_on_one_gpu(world, transport):
+    """The DeviceOps path (K1/K3 per shard, all-to-all + phb_regroup or the
+    fused CUDA-IPC peer scatter, K4 on owned partitions, seed all_gather, K5)
+    with `world` ranks sharing one GPU over gloo: every rank's bytes equal
+    the single-GPU build."""
     import torch.multiprocessing as mp
 
     import paper_2404_18497_b200 as phb
@@ -105,7 +107,8 @@ def test_device_sharded_build_gloo_on_one_gpu(world):
     cfg_kw = dict(lambda_=7.0, partition_size=2500.0, encoder="ic-r")
     d = tempfile.mkdtemp()
     out = os.path.join(d, "blob")
-    mp.spawn(_dev_worker, args=(world, os.path.join(d, "rdv"), keys, cfg_kw, out), nprocs=world)
+    mp.spawn(_dev_worker, args=(world, os.path.join(d, "rdv"), keys, cfg_kw, out, transport),
+             nprocs=world)
     want = phb.build(keys, phb.BuildConfig(**cfg_kw))
     for r in range(world):
         assert np.load(out + f".{r}.npy").tobytes() == want.serialize()
