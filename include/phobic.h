@@ -194,6 +194,10 @@ int phb_ipc_open(const uint8_t* handle64, void** dptr);
 int phb_ipc_close(void* dptr);
 int phb_sync(void* stream);
 
+/* Search work counters (only in builds with -DPHB_STATS; else returns
+ * PHB_E_ARGS): 16 u64 to HOST out16; reset != 0 clears them. */
+int phb_search_stats(unsigned long long* out16, int reset);
+
 /* Synthetic distinct 64-bit keys for benchmarks: out[i] = mix64(offset + i)
  * (mix64 is a bijection on u64, so keys are distinct for distinct i). The
  * host restatement is keygen.synth_u64. Not a reference interface: bench

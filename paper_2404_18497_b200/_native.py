@@ -50,6 +50,7 @@ SIGNATURES = {
     "phb_ipc_open": [P, P],
     "phb_ipc_close": [P],
     "phb_sync": [P],
+    "phb_search_stats": [P, INT],
 }
 OTHER = {
     "phb_version": ([], ctypes.c_char_p),

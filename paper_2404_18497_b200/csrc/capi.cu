@@ -25,6 +25,8 @@ int num_sms() {
   return cached[dev];
 }
 
+int search_stats(unsigned long long* out16, int reset);
+
 int launch_decode(const uint8_t* blob, int64_t ncols, const int64_t* host_info, int64_t nparts,
                   uint32_t B, int mono, uint64_t* seeds, cudaStream_t st);
 
@@ -345,6 +347,10 @@ int phb_ipc_open(const uint8_t* handle64, void** dptr) {
 int phb_ipc_close(void* dptr) { return (int)cudaIpcCloseMemHandle(dptr); }
 
 int phb_sync(void* stream) { return (int)cudaStreamSynchronize(S(stream)); }
+
+int phb_search_stats(unsigned long long* out16, int reset) {
+  return search_stats(out16, reset);
+}
 
 int phb_synth_keys(uint64_t* out, int64_t n, uint64_t offset, void* stream) {
   if (n < 0) return PHB_E_ARGS;

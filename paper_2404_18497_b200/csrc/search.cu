@@ -112,6 +112,16 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 extern __shared__ uint32_t smem[];
 
+#ifdef PHB_STATS
+// [0] G=1 batches [1] G=2 batches [2] G=4 batches [3] small key-steps
+// [4] generic s-iterations [5] generic key-rounds [6] singletons [7] buckets k>=2
+// [8] early exits [9] generic d-searches
+__device__ unsigned long long g_stats[16];
+#define STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define STAT(i, v) do { } while (0)
+#endif
+
 __device__ __forceinline__ void mark(uint32_t occ, uint32_t slot, uint32_t m, int tag = 0) {
 #ifdef PHB_DEBUG
   if (slot >= m) { printf("mark: slot %u m %u tag %d\n", slot, m, tag); __trap(); }
@@ -249,6 +259,8 @@ __device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint
   uint32_t p0 = 0;  // this lane's base position (k <= 32)
 #pragma unroll 1
   for (int64_t s = s_begin;; ++s) {
+    STAT(4, 1);
+    STAT(5, (k + 31) / 32);
     const int64_t pbase = s * (int64_t)m;
     if (s > 0 && pbase > cap) return {0, trials, 2};  // _kernels.py:324-328
     const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
@@ -363,6 +375,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   const int64_t s_full = cap >= (int64_t)m - 1 ? (cap - (int64_t)m + 1) / (int64_t)m : -1;
 #pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
+    STAT(G == 1 ? 0 : (G == 2 ? 1 : 2), 1);
     const int64_t s = s_next + grp;
     const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
     const uint32_t p = position(key, g, m);
@@ -421,6 +434,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     uint32_t pnext = mypos[0];
 #pragma unroll 1
     for (uint32_t i = 0; i < k; ++i) {
+      STAT(3, 1);
       const uint32_t pi = pnext;
       if (PHB_PREFETCH) pnext = mypos[i + 1 < k ? i + 1 : i];
       else if (i + 1 < k) pnext = mypos[i + 1];
@@ -633,6 +647,7 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
       const uint32_t k = smem[cnt + b];
       const uint64_t* kl = a.glo + kb + (smem[endp + b] - k);
       BucketResult res;
+      STAT(k == 1 ? 6 : 7, 1);
       if (k == 1) {
         // singleton: first free slot cyclically from the s = 0 base; no cap
         // (_kernels.py:300-310)
@@ -680,6 +695,20 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
       if (a.part_trials) a.part_trials[row] = ptrials;
     }
   }
+}
+
+int search_stats(unsigned long long* out16, int reset) {
+#ifdef PHB_STATS
+  PHB_CUDA_TRY(cudaMemcpyFromSymbol(out16, g_stats, sizeof(unsigned long long) * 16));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    PHB_CUDA_TRY(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
+  }
+  return 0;
+#else
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  return 1003;
+#endif
 }
 
 int launch_search(const SearchArgs& a, cudaStream_t st) {
