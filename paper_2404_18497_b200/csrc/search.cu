@@ -40,6 +40,9 @@ namespace phb {
 #ifndef PHB_MASKTAB
 #define PHB_MASKTAB 1
 #endif
+#ifndef PHB_MINB
+#define PHB_MINB 8  // CTAs of 4 warps per SM the register budget targets
+#endif
 #ifndef PHB_LDS64
 #define PHB_LDS64 0  // measured slower (round 1)
 #endif
@@ -84,7 +87,10 @@ __host__ __device__ inline SmemPlan smem_plan(int64_t m_max, uint32_t bcount) {
   p.sh_w = SH;       // shist + srun as u16
   p.pos_w = PMAX / 2;  // u16 base positions
   p.occ_w = (p.occ_w + 3) & ~3;  // keep the mask table that follows 16-byte aligned
-  p.total_w = p.occ_w + 96 + p.scr_w + 2 * p.cnt_w + p.ord_w + p.sh_w + p.pos_w;
+  // the bucket-order scratch (shist/srun) is dead before the search state
+  // (mask table, collision map, positions) is written: they share one region
+  const int search_w = 96 + p.scr_w + p.pos_w;
+  p.total_w = p.occ_w + 2 * p.cnt_w + p.ord_w + (p.sh_w > search_w ? p.sh_w : search_w);
   p.total_w = (p.total_w + 3) & ~3;  // 16-byte aligned warp regions (LDS.128)
   return p;
 }
@@ -561,19 +567,20 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   return {0, trials, -1};
 }
 
-__global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan plan) {
+__global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, SmemPlan plan) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t B = a.bcount;
   const uint32_t occ = wid * plan.total_w;
-  const uint32_t dmask = occ + plan.occ_w;  // 96-word "past dmax" table for dmax = m - 1
-  const uint32_t scr = dmask + 96;
-  const uint32_t cnt = scr + plan.scr_w;
+  const uint32_t cnt = occ + plan.occ_w;
   const uint32_t endp = cnt + plan.cnt_w;
   uint16_t* const sm16 = reinterpret_cast<uint16_t*>(smem);
   uint16_t* const order = sm16 + 2 * (endp + plan.cnt_w);
-  uint16_t* const shist = order + 2 * plan.ord_w;
+  const uint32_t shared_x = endp + plan.cnt_w + plan.ord_w;  // bucket-order / search union
+  uint16_t* const shist = sm16 + 2 * shared_x;
   uint16_t* const srun = shist + SH;
-  uint16_t* const pos16 = srun + SH;
+  const uint32_t dmask = shared_x;      // 96-word "past dmax" table for dmax = m - 1
+  const uint32_t scr = dmask + 96;      // self-collision map (m bits)
+  uint16_t* const pos16 = sm16 + 2 * (scr + plan.scr_w);
   const int64_t nrange = a.p_hi - a.p_lo;
   const uint64_t g0 = mix64(POSITION_SALT);  // s = 0
   const int64_t cap = a.seed_cap;
@@ -624,6 +631,11 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
     const uint32_t occ_used = min((uint32_t)plan.occ_w, (2 * m) / 32 + 104);
 #pragma unroll 1
     for (uint32_t w = lane; w < occ_used; w += 32) smem[occ + w] = 0;
+    __syncwarp();
+
+    const uint32_t nb = bucket_order(cnt, B, a.tie_desc, maxsz, order, shist, srun, lane);
+    __syncwarp();
+    // search state (overwrites the bucket-order scratch)
     const uint32_t scr_used = m / 32 + 2;
 #pragma unroll 1
     for (uint32_t w = lane; w < scr_used; w += 32) smem[scr + w] = 0;
@@ -632,9 +644,6 @@ __global__ void __launch_bounds__(WARPS * 32, 8) k_search(SearchArgs a, SmemPlan
       const int64_t lt = (int64_t)m - 1 - 32 * (int64_t)w;  // last valid bit of word w
       smem[dmask + w] = lt < 0 ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
     }
-    __syncwarp();
-
-    const uint32_t nb = bucket_order(cnt, B, a.tie_desc, maxsz, order, shist, srun, lane);
     __syncwarp();
 
     // ---- seed search, bucket by bucket (_kernels.py:295-369)
