@@ -195,7 +195,7 @@ int phb_ipc_close(void* dptr);
 int phb_sync(void* stream);
 
 /* Search work counters (only in builds with -DPHB_STATS; else returns
- * PHB_E_ARGS): 16 u64 to HOST out16; reset != 0 clears them. */
+ * PHB_E_ARGS): 32 u64 to HOST out16; reset != 0 clears them. */
 int phb_search_stats(unsigned long long* out16, int reset);
 
 /* Synthetic distinct 64-bit keys for benchmarks: out[i] = mix64(offset + i)

@@ -122,10 +122,22 @@ extern __shared__ uint32_t smem[];
 // [0] G=1 batches [1] G=2 batches [2] G=4 batches [3] small key-steps
 // [4] generic s-iterations [5] generic key-rounds [6] singletons [7] buckets k>=2
 // [8] early exits [9] generic d-searches
-__device__ unsigned long long g_stats[16];
-#define STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], (unsigned long long)(v)); } while (0)
+// [10] cycles: prologue (histogram, grouping, order) [11] singletons
+// [12] small k (<= 32) [13] generic (k > 32 or m > 3072) [14] queue + output
+// [16..18] cycles for k in 2..8 / 9..16 / 17..32, [19..21] their bucket counts,
+// [22..24] their seeds tested (s* + 1)
+// Counters live per warp in shared memory (lane 0 only, no contention) and
+// are flushed to g_stats once per warp at kernel exit, so the counting does
+// not perturb the timings it records.
+__device__ unsigned long long g_stats[32];
+__shared__ unsigned long long s_stats[4][32];
+#define STAT(i, v) do { if ((threadIdx.x & 31) == 0) s_stats[threadIdx.x >> 5][i] += (unsigned long long)(v); } while (0)
+#define TSTAMP(t) const long long t = clock64()
+#define TACC(i, t0) STAT(i, clock64() - (t0))
 #else
 #define STAT(i, v) do { } while (0)
+#define TSTAMP(t) do { } while (0)
+#define TACC(i, t0) do { } while (0)
 #endif
 
 __device__ __forceinline__ void mark(uint32_t occ, uint32_t slot, uint32_t m, int tag = 0) {
@@ -584,13 +596,24 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
   const int64_t nrange = a.p_hi - a.p_lo;
   const uint64_t g0 = mix64(POSITION_SALT);  // s = 0
   const int64_t cap = a.seed_cap;
+#ifdef PHB_STATS
+  if (lane == 0)
+    for (int i = 0; i < 32; ++i) s_stats[wid][i] = 0;
+#endif
 
 #pragma unroll 1
   for (;;) {
+    TSTAMP(tq);
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(a.queue, 1u);
     t = __shfl_sync(FULL, t, 0);
-    if ((int64_t)t >= nrange) break;
+    if ((int64_t)t >= nrange) {
+#ifdef PHB_STATS
+      if (lane == 0)
+        for (int i = 0; i < 32; ++i) atomicAdd(&g_stats[i], s_stats[wid][i]);
+#endif
+      break;
+    }
     const int64_t j = a.p_lo + t;
     const int64_t row = j - a.out_base;
     const int64_t kb = a.key_off[j];
@@ -603,6 +626,8 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
       continue;
     }
 
+    TACC(14, tq);
+    TSTAMP(tp);
     // ---- bucket histogram + counting sort into glo (_kernels.py:252-266)
 #pragma unroll 1
     for (uint32_t b = lane; b <= B; b += 32) smem[cnt + b] = 0;
@@ -646,6 +671,7 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     }
     __syncwarp();
 
+    TACC(10, tp);
     // ---- seed search, bucket by bucket (_kernels.py:295-369)
     int64_t ptrials = 0;
     uint8_t status = 0;
@@ -657,6 +683,7 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
       const uint64_t* kl = a.glo + kb + (smem[endp + b] - k);
       BucketResult res;
       STAT(k == 1 ? 6 : 7, 1);
+      TSTAMP(tb);
       if (k == 1) {
         // singleton: first free slot cyclically from the s = 0 base; no cap
         // (_kernels.py:300-310)
@@ -687,6 +714,15 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
       } else {
         res = generic_bucket(occ, scr, pos16, k, kl, m, cap, 0, 0, lane);
       }
+      TACC(k == 1 ? 11 : ((small_ok && k <= 32) ? 12 : 13), tb);
+#ifdef PHB_STATS
+      if (small_ok && k >= 2 && k <= 32 && res.status == 0) {
+        const int cls = k <= 8 ? 0 : (k <= 16 ? 1 : 2);
+        TACC(16 + cls, tb);
+        STAT(19 + cls, 1);
+        STAT(22 + cls, res.seed / m + 1);
+      }
+#endif
       if (res.status > 0) {
         status = (uint8_t)res.status;
         break;
@@ -708,14 +744,14 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
 
 int search_stats(unsigned long long* out16, int reset) {
 #ifdef PHB_STATS
-  PHB_CUDA_TRY(cudaMemcpyFromSymbol(out16, g_stats, sizeof(unsigned long long) * 16));
+  PHB_CUDA_TRY(cudaMemcpyFromSymbol(out16, g_stats, sizeof(unsigned long long) * 32));
   if (reset) {
-    unsigned long long z[16] = {0};
+    unsigned long long z[32] = {0};
     PHB_CUDA_TRY(cudaMemcpyToSymbol(g_stats, z, sizeof(z)));
   }
   return 0;
 #else
-  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  for (int i = 0; i < 32; ++i) out16[i] = 0;
   return 1003;
 #endif
 }
