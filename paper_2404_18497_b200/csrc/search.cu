@@ -34,37 +34,13 @@
 
 namespace phb {
 
-#ifndef PHB_LDS128
-#define PHB_LDS128 0  // measured slower (round 1): 4-way switch + code size
-#endif
-#ifndef PHB_MASKTAB
-#define PHB_MASKTAB 1
-#endif
+// Register budget: CTAs of 4 warps per SM (8 -> 64 registers, 32 warps/SM).
+// Variants measured slower at C2 (round 1, tools/variant_bench.py) and
+// removed: 64/128-bit window loads, key pairs folded with 3-input ORs,
+// IMAD.WIDE funnel shifts, closed-form batch resolution, conflict-free
+// multi-seed layout, out-of-line generic path, no G = 2 batches.
 #ifndef PHB_MINB
-#define PHB_MINB 8  // CTAs of 4 warps per SM the register budget targets
-#endif
-#ifndef PHB_LDS64
-#define PHB_LDS64 0  // measured slower (round 1)
-#endif
-#ifndef PHB_PREFETCH
-#define PHB_PREFETCH 1
-#endif
-#ifndef PHB_PAIR
-#define PHB_PAIR 0  // measured slower (round 1)
-#endif
-#ifndef PHB_FASTRES
-#define PHB_FASTRES 0  // measured slower (round 1): code size
-#endif
-#ifndef PHB_USE_G2
-#define PHB_USE_G2 1
-#endif
-#ifndef PHB_NOINLINE_GENERIC
-#define PHB_NOINLINE_GENERIC 0
-#endif
-#if PHB_NOINLINE_GENERIC
-#define PHB_COLD __noinline__
-#else
-#define PHB_COLD
+#define PHB_MINB 8
 #endif
 
 constexpr int SH = 256;     // size classes of the counting-sort bucket order
@@ -218,7 +194,7 @@ __device__ uint32_t bucket_order(uint32_t cnt, uint32_t B, int tie_desc, uint32_
 // First displacement d in [0, dmax] with every key's slot free, or -1.
 // Base positions come from the staged u16 list (k <= PMAX) or are re-derived
 // from the key scratch (larger buckets).
-__device__ PHB_COLD int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t k,
+__device__ int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t k,
                                           int64_t dmax, const uint64_t* kl, uint64_t g,
                                           uint32_t m, int lane) {
   const uint32_t nwd = (uint32_t)((dmax + 32) >> 5);  // words of the valid mask
@@ -267,7 +243,7 @@ struct BucketResult {
 
 // Generic single-s search (any k, any m): the reference loop of
 // _kernels.py:312-369 with each s tested by the whole warp.
-__device__ PHB_COLD BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos16, uint32_t k,
+__device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos16, uint32_t k,
                                        const uint64_t* kl, uint32_t m, int64_t cap,
                                        int64_t s_begin, int64_t trials, int lane) {
   const uint32_t R = (k + 31) >> 5;
@@ -389,8 +365,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   const uint64_t key = act ? kl[gl] : 0ull;
   uint16_t* const mypos = pos16 + grp * L;
   const uint32_t wb = (uint32_t)gl * WPL;
-  // seeds s <= s_full sweep every displacement (dmax = m - 1, below the cap)
-  const int64_t s_full = cap >= (int64_t)m - 1 ? (cap - (int64_t)m + 1) / (int64_t)m : -1;
 #pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
     STAT(G == 1 ? 0 : (G == 2 ? 1 : 2), 1);
@@ -411,7 +385,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     // start from "displacements past dmax are occupied": the partition's
     // mask table (dmax = m - 1) or, near the seed cap, computed here
     uint32_t acc[WPL];
-    if (PHB_MASKTAB && dmax == (int64_t)m - 1) {
+    if (dmax == (int64_t)m - 1) {
 #pragma unroll
       for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : smem[dmask + wb + t];
     } else {
@@ -422,31 +396,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         acc[t] = (dead_group || lt < 0) ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
       }
     }
-#if PHB_PAIR
-    // keys two at a time (an odd k repeats its last key; OR is idempotent),
-    // folding both windows with one 3-input OR
-#pragma unroll 1
-    for (uint32_t i = 0; i < k; i += 2) {
-      const uint32_t pa = mypos[i];
-      const uint32_t pb = mypos[i + 1 < k ? i + 1 : i];
-      const uint32_t sha = pa & 31, shb = pb & 31;
-      const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
-      uint32_t xa = smem[Wa], xb = smem[Wb];
-#pragma unroll
-      for (int t = 0; t < WPL; ++t) {
-        const uint32_t ya = smem[Wa + t + 1], yb = smem[Wb + t + 1];
-        acc[t] |= __funnelshift_r(xa, ya, sha) | __funnelshift_r(xb, yb, shb);
-        xa = ya;
-        xb = yb;
-      }
-      if ((i & 2) == 2) {  // every 4 keys: stop once no displacement can survive
-        uint32_t all = FULL;
-#pragma unroll
-        for (int t = 0; t < WPL; ++t) all &= acc[t];
-        if (__all_sync(FULL, all == FULL)) break;
-      }
-    }
-#else
     // the next key's base position is loaded one iteration ahead, so its
     // shared-memory latency hides behind the current key's window loads
     uint32_t pnext = mypos[0];
@@ -454,41 +403,15 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     for (uint32_t i = 0; i < k; ++i) {
       STAT(3, 1);
       const uint32_t pi = pnext;
-      if (PHB_PREFETCH) pnext = mypos[i + 1 < k ? i + 1 : i];
-      else if (i + 1 < k) pnext = mypos[i + 1];
+      pnext = mypos[i + 1 < k ? i + 1 : i];
       const uint32_t sh = pi & 31;
       const uint32_t W = occ + (pi >> 5) + wb;
-      if constexpr (PHB_LDS64 && (WPL % 2) == 0) {
-        // wb is even for G = 4 / 2, so the word parity of W is warp-uniform:
-        // read the lane's WPL + 1 words with 64-bit loads (one 32-bit load
-        // first when W is odd), then the same funnel-shift block
-        uint32_t w[WPL + 2];
-        if (W & 1u) {
-          w[0] = smem[W];
+      uint32_t x = smem[W];
 #pragma unroll
-          for (int c = 0; c < WPL / 2; ++c) {
-            const uint2 v = *reinterpret_cast<const uint2*>(&smem[W + 1 + 2 * c]);
-            w[1 + 2 * c] = v.x;
-            w[2 + 2 * c] = v.y;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c <= WPL / 2; ++c) {
-            const uint2 v = *reinterpret_cast<const uint2*>(&smem[W + 2 * c]);
-            w[2 * c] = v.x;
-            w[2 * c + 1] = v.y;
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < WPL; ++t) acc[t] |= __funnelshift_r(w[t], w[t + 1], sh);
-      } else {
-        uint32_t x = smem[W];
-#pragma unroll
-        for (int t = 0; t < WPL; ++t) {
-          const uint32_t y = smem[W + t + 1];
-          acc[t] |= __funnelshift_r(x, y, sh);
-          x = y;
-        }
+      for (int t = 0; t < WPL; ++t) {
+        const uint32_t y = smem[W + t + 1];
+        acc[t] |= __funnelshift_r(x, y, sh);
+        x = y;
       }
       if ((i & 3) == 3) {
         uint32_t all = FULL;
@@ -497,7 +420,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         if (__all_sync(FULL, all == FULL)) break;
       }
     }
-#endif
     // this lane's first valid displacement (d <= dmax), or -1
     uint32_t sat = FULL;
 #pragma unroll
@@ -509,34 +431,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
 #pragma unroll
       for (int t = WPL - 1; t >= 0; --t)
         if (acc[t] != FULL) myd = 32 * (int64_t)(wb + t) + (__ffs(~acc[t]) - 1);
-    }
-    if (PHB_FASTRES && s_next > 0 && s_next + G - 1 <= s_full) {
-      // common case: no seed of the batch touches the cap or s = 0. The
-      // sequential loop's outcome in closed form: seeds before the first
-      // group with a valid displacement either self-collided (k trials) or
-      // swept all m displacements (k*m trials).
-      uint32_t collm = 0, foundm = 0;
-#pragma unroll
-      for (int gi = 0; gi < G; ++gi) {
-        collm |= (uint32_t)(((cball >> (gi * L)) & LMASK) != 0) << gi;
-        foundm |= (uint32_t)(((fball >> (gi * L)) & LMASK) != 0) << gi;
-      }
-      const int gw = foundm ? __ffs(foundm) - 1 : G;
-      const int ncoll = __popc(collm & ((1u << gw) - 1u));
-      trials += (int64_t)k * ncoll + (int64_t)k * m * (gw - ncoll);
-      if (foundm) {
-        const int64_t d = __shfl_sync(FULL, myd, __ffs((fball >> (gw * L)) & LMASK) - 1 + gw * L);
-        trials += (int64_t)k * (d + 1);
-        if (grp == gw && act) {
-          uint32_t slot = p + (uint32_t)d;
-          if (slot >= m) slot -= m;
-          mark(occ, slot, m, 100 * G + (int)k);
-        }
-        return {(s_next + gw) * (int64_t)m + d, trials, 0};
-      }
-      s_next += G;
-      __syncwarp();
-      continue;
     }
     // general resolution (s = 0 duplicate check, seed cap): seed by seed
 #pragma unroll 1
@@ -700,16 +594,14 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
         // then batches of G seeds; one call site per instantiation keeps the
         // kernel's instruction footprint small
         int64_t s_next = 0;
-        const uint32_t kg1 = PHB_USE_G2 ? 16u : 8u;  // larger buckets stay single-seed
+        const uint32_t kg1 = 16u;  // larger buckets stay single-seed
         res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, 0, k > kg1 ? (1 << 30) : 1,
                               lane);
         if (res.status < 0) {
           if (k <= 8)
             res = small_bucket<4>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
-#if PHB_USE_G2
           else
             res = small_bucket<2>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
-#endif
         }
       } else {
         res = generic_bucket(occ, scr, pos16, k, kl, m, cap, 0, 0, lane);
