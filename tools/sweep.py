@@ -1,7 +1,8 @@
-"""Secondary BASELINE configs (C1, C4 lambda sweep, C5 strings): device build
-time, bits/key, query rate. Prints one JSON line per config.
+"""Secondary BASELINE configs (C1, C3 1B keys on one GPU, C4 lambda sweep, C5
+strings): device build time, bits/key, query rate, bijection. Prints one JSON
+line per config.
 
-    python tools/sweep.py [--configs C1,C4,C5] [--n4 100000000] [--n5 100000000]
+    python tools/sweep.py [--configs C1,C3,C4,C5] [--n3 1000000000] [--n4 100000000] [--n5 100000000]
 """
 
 import argparse
@@ -63,6 +64,7 @@ def report(name, n, cfg, ms, res, q_ms, ok, extra=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C4,C5")
+    ap.add_argument("--n3", type=int, default=1_000_000_000)
     ap.add_argument("--n4", type=int, default=100_000_000)
     ap.add_argument("--n5", type=int, default=100_000_000)
     a = ap.parse_args()
@@ -76,6 +78,18 @@ def main():
         ms, res, eng = timed_build(dk, cfg, reps=10)
         q, ok = query_rate(res, eng, cfg, dk)
         report("C1 1M u64 lambda=5 IC-C", n, cfg, ms, res, q, ok)
+    if "C3" in cfgs:
+        # BASELINE configs[2] is 1B keys over 2/4/8 GPUs; one B200 holds it whole
+        # (keys 8 GB + build buffers ~20 GB), which is the G = 1 point of that sweep
+        n = a.n3
+        keys = synth_u64_device(n, 0)
+        dk = DeviceKeys(n, keys64=keys)
+        cfg = phb.BuildConfig(lambda_=9.0, partition_size=2500.0, encoder="ic-c")
+        ms, res, eng = timed_build(dk, cfg, reps=2)
+        q, ok = query_rate(res, eng, cfg, dk)
+        report(f"C3 {n // 1_000_000}M u64 lambda=9 IC-C, 1 GPU", n, cfg, ms, res, q, ok)
+        del keys, dk, res, eng
+        torch.cuda.empty_cache()
     if "C4" in cfgs:
         n = a.n4
         keys = synth_u64_device(n, 0)
