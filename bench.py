@@ -43,7 +43,8 @@ PSIZE = 2500.0
 ENCODER = "ic-c"
 PUBLISHED_NS_PER_KEY = 28.0  # PHOBIC-GPU lambda=9 IC-C, RTX 3090
 ALGO_BYTES = {"total": 28, "hash_count": 8, "scatter": 18, "search": 10}  # SURVEY.md §8(d), per key
-KERNELS_PER_BUILD = 11  # hash_count, layout, scatter, search, 7 encode kernels
+KERNELS_PER_BUILD = 12  # hash_count, layout, cursor_init, scatter, search, 7 encode kernels
+# (profiles/r1_launches_c2.csv: the ncu launch list of one build, plus two torch zero-fills)
 
 
 def _peaks():
@@ -327,6 +328,13 @@ def run_gpu(args):
             traffic = json.loads(tp.read_text()).get("bytes_per_launch")
         except Exception:
             traffic = None
+    sm = None
+    sp = ROOT / "profiles" / "search_sm_c2.json"
+    if sp.exists():
+        try:
+            sm = json.loads(sp.read_text())
+        except Exception:
+            sm = None
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world,
@@ -355,7 +363,14 @@ def run_gpu(args):
                      "note": "search is issue/latency bound (integer + shared-memory bit "
                              "ops), not HBM bound; algorithmic bytes = 10 B/key read "
                              "(SURVEY.md §8(d)); see passes for the HBM-bound kernels",
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback",
+                     # the bound that does apply to k_search (ncu --set full, same workload)
+                     "sm": None if sm is None else {
+                         "issue_active_pct": round(sm["issue_active_pct"], 1),
+                         "alu_pipe_pct": round(sm["alu_pipe_pct_elapsed"], 1),
+                         "shared_lsu_pct": round(sm["lsu_shared_wavefront_pct_elapsed"], 1),
+                         "warp_instructions_per_key": round(sm["warp_instructions"] / 1e8, 1),
+                         "source": "profiles/search_sm_c2.json"}},
         "passes": passes,
         "clocks": clocks,
     }
