@@ -152,6 +152,21 @@ int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64
               const double* entries, int32_t bcount, const uint64_t* seeds, int64_t s_sj,
               int64_t s_sb, int64_t* out, void* stream);
 
+/* K7e: batched query reading seeds straight from the encoded seed section
+ * (Compact fields, Rice lows + sampled select over the unary highs:
+ * CompactVector.get / RiceVector.get, encoders.py:89-99, :224-230, :129-154),
+ * no decoded matrix. section: DEVICE copy of the serialized seed section's
+ * encoder blocks; col_info: DEVICE int64[num_enc][8] = {kind (0 Compact,
+ * 1 Rice), width or b, count, payload byte, highs byte, highs_nbits,
+ * samples byte, nsamples}, byte offsets relative to section. Interleaved:
+ * num_enc == bcount, encoder b-1 indexed by partition; mono: one encoder
+ * indexed j*bcount + b-1. */
+int phb_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
+                      int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
+                      const int64_t* key_off, const double* entries, int32_t bcount,
+                      const uint8_t* section, const int64_t* col_info, int32_t num_enc,
+                      int32_t mono, int64_t* out, void* stream);
+
 /* K8: bijection check onto [0, n): bitmap (ceil(n/32) u32, zeroed by
  * caller) and bad_flag (one u32, zeroed) set to 1 on a repeat or an
  * out-of-range output. Bijection <=> nq == n and bad_flag == 0. */

@@ -38,6 +38,7 @@ SIGNATURES = {
     "phb_encode_write": [P, I64, I32, I32, I32, P, I64, P, P, P, SZ, P],
     "phb_decode_seeds": [P, I64, P, I64, I32, I32, P, P],
     "phb_query": [P, P, P, I64, U64, I64, I64, P, P, I32, P, I64, I64, P, P],
+    "phb_query_encoded": [P, P, P, I64, U64, I64, I64, P, P, I32, P, P, I32, I32, P, P],
     "phb_verify": [P, I64, I64, P, P, P],
     "phb_offsets_from_deltas": [P, I64, I64, P, P],
     "phb_device_sms": [],

@@ -303,6 +303,18 @@ int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64
                       entries, (uint32_t)bcount, seeds, s_sj, s_sb, out, S(stream));
 }
 
+int phb_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
+                      int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
+                      const int64_t* key_off, const double* entries, int32_t bcount,
+                      const uint8_t* section, const int64_t* col_info, int32_t num_enc,
+                      int32_t mono, int64_t* out, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (nparts < 1 || !section || !col_info) return PHB_E_ARGS;
+  if (mono ? num_enc != 1 : num_enc != bcount) return PHB_E_ARGS;
+  return launch_query_encoded(buf, offsets, keys64, nq, seed, n, nparts, key_off, entries,
+                              (uint32_t)bcount, section, col_info, mono, out, S(stream));
+}
+
 int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad_flag,
                void* stream) {
   return launch_verify(out, nq, n, bitmap, bad_flag, S(stream));

@@ -59,6 +59,130 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- K7e: query straight from the encoded seed section (no decoded matrix).
+// Replaces CompactVector.get (encoders.py:89-99), RiceVector.get
+// (encoders.py:224-230) with Select.select1 / next_one (encoders.py:129-154),
+// and InterleavedSeeds.seed_at / MonoSeeds index maps (encoders.py:305-341)
+// inside query_many_kernel. The section stays in HBM/L2 at its serialized
+// size (~bits/key * n / 8), e.g. 27 MB at C2 instead of a 89 MB matrix.
+struct ECol {  // one encoder of the section, byte offsets relative to the section blob
+  int64_t kind, param, count, pay_byte, highs_byte, highs_nbits, samples_byte, nsamples;
+};
+
+#ifndef PHB_EBITS_BYTES
+#define PHB_EBITS_BYTES 0
+#endif
+// little-endian bit field [addr, addr + nbits), nbits <= 64. Default: two
+// aligned 64-bit loads (the section blob is 8-byte aligned and zero padded);
+// PHB_EBITS_BYTES: byte loads.
+__device__ __forceinline__ uint64_t ebits(const uint8_t* __restrict__ blob, uint64_t addr,
+                                          int nbits) {
+  if (nbits <= 0) return 0;
+#if PHB_EBITS_BYTES
+  const uint8_t* p = blob + (addr >> 3);
+  const int sh = (int)(addr & 7);
+  const int need = (sh + nbits + 7) >> 3;  // <= 9
+  uint64_t lo = 0, hi = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (i < need) lo |= (uint64_t)__ldg(p + i) << (8 * i);
+  if (need > 8) hi = __ldg(p + 8);
+  const uint64_t v = (lo >> sh) | (sh ? (hi << (64 - sh)) : 0ull);
+#else
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(blob) + (addr >> 6);
+  const int sh = (int)(addr & 63);
+  uint64_t v = __ldg(w) >> sh;
+  if (sh + nbits > 64) v |= __ldg(w + 1) << (64 - sh);
+#endif
+  return nbits >= 64 ? v : (v & ((1ull << nbits) - 1));
+}
+
+__device__ __forceinline__ uint32_t ehigh_word(const uint8_t* blob, const ECol& d, int64_t w) {
+  const int64_t nb = d.highs_nbits - 32 * w;
+  if (nb <= 0) return 0;
+  return (uint32_t)ebits(blob, 8ull * d.highs_byte + 32ull * w, nb < 32 ? (int)nb : 32);
+}
+
+// Select.select1: position of the (k+1)-th one (k >= 0)
+__device__ int64_t eselect1(const uint8_t* blob, const ECol& d, int64_t k) {
+  const int64_t spos = (int64_t)ebits(blob, 8ull * d.samples_byte + 64ull * (k >> 10), 64);
+  int need = (int)(k & 1023) + 1;
+  int64_t w = spos >> 5;
+  uint32_t word = ehigh_word(blob, d, w) & (0xffffffffu << (spos & 31));
+  for (;;) {
+    const int c = __popc(word);
+    if (c >= need) {
+      for (int r = 1; r < need; ++r) word &= word - 1;
+      return 32 * w + (__ffs(word) - 1);
+    }
+    need -= c;
+    word = ehigh_word(blob, d, ++w);
+  }
+}
+
+// Select.next_one: first one at index >= pos
+__device__ int64_t enext_one(const uint8_t* blob, const ECol& d, int64_t pos) {
+  int64_t w = pos >> 5;
+  uint32_t word = ehigh_word(blob, d, w) & (0xffffffffu << (pos & 31));
+  while (!word) word = ehigh_word(blob, d, ++w);
+  return 32 * w + (__ffs(word) - 1);
+}
+
+__device__ __forceinline__ uint64_t eget(const uint8_t* blob, const ECol* dp, int64_t i) {
+  // only {kind, param} and {count, payload} are read for Compact columns
+  const longlong2 kp = __ldg(reinterpret_cast<const longlong2*>(dp));
+  const int64_t pay = __ldg(&dp->pay_byte);
+  if (kp.x == 0) {  // CompactVector.get
+    const int w = (int)kp.y;
+    return w ? ebits(blob, 8ull * pay + (uint64_t)i * w, w) : 0ull;
+  }
+  const int b = (int)kp.y;  // RiceVector.get
+  const uint64_t low = b ? ebits(blob, 8ull * pay + (uint64_t)i * b, b) : 0ull;
+  if (b >= 64) return low;
+  const ECol d = *dp;
+  const int64_t prev = i > 0 ? eselect1(blob, d, i - 1) : -1;
+  const int64_t pos = enext_one(blob, d, prev + 1);
+  return ((uint64_t)(pos - prev - 1) << b) | low;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    k_query_enc(const uint8_t* __restrict__ buf, const int64_t* __restrict__ offsets,
+                const uint64_t* __restrict__ keys64, int64_t nq, uint64_t seed, int64_t n,
+                uint64_t nparts, const int64_t* __restrict__ key_off,
+                const double* __restrict__ entries, uint32_t bcount,
+                const uint8_t* __restrict__ sec, const ECol* __restrict__ cols, int mono,
+                int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    Hash128 h;
+    if (MODE == 0) {
+      h = murmur3_u64(__ldg(keys64 + i), seed);
+    } else {
+      int64_t a = __ldg(offsets + i), b = __ldg(offsets + i + 1);
+      h = murmur3_bytes(buf + a, b - a, seed);
+    }
+    const uint64_t j = mulhi(h.hi, nparts);
+    const int64_t offj = __ldg(key_off + j);
+    const int64_t m = __ldg(key_off + j + 1) - offj;
+    int64_t r;
+    if (m <= 0) {
+      r = offj < n ? offj : n - 1;
+    } else {
+      const uint32_t b = bucket_of(entries, h.hi, bcount);
+      const uint64_t p = mono ? eget(sec, cols, (int64_t)j * bcount + (b - 1))
+                              : eget(sec, cols + (b - 1), (int64_t)j);
+      const uint64_t mu = (uint64_t)m;
+      const uint64_t s = p / mu;
+      const uint64_t d = p - s * mu;
+      uint64_t pos = mulhi(mix64(h.lo ^ mix64(s ^ POSITION_SALT)), mu) + d;
+      if (pos >= mu) pos -= mu;
+      r = offj + (int64_t)pos;
+    }
+    out[i] = r;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_verify(const int64_t* __restrict__ out, int64_t nq,
                                                 int64_t n, uint32_t* __restrict__ bitmap,
                                                 uint32_t* __restrict__ bad) {
@@ -99,6 +223,23 @@ int launch_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* key
   else
     k_query<1><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
                                   key_off, entries, bcount, seeds, s_sj, s_sb, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
+                         int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
+                         const int64_t* key_off, const double* entries, uint32_t bcount,
+                         const uint8_t* section, const int64_t* cols, int mono, int64_t* out,
+                         cudaStream_t st) {
+  if (nq <= 0) return 0;
+  const int g = qgrid(nq);
+  const ECol* c = reinterpret_cast<const ECol*>(cols);
+  if (keys64)
+    k_query_enc<0><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
+                                      entries, bcount, section, c, mono, out);
+  else
+    k_query_enc<1><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
+                                      entries, bcount, section, c, mono, out);
   return (int)cudaGetLastError();
 }
 

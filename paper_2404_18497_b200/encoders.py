@@ -163,8 +163,9 @@ def _parse_encoder(data: bytes, at: int) -> tuple[Encoder, int, tuple]:
 
 
 def _col_info(encs, geo_at0=None) -> np.ndarray:
-    """8 int64 per encoder for phb_decode_seeds, relative to a section that
-    starts with the first block at byte 0 of a blob built by _section_blob."""
+    """8 int64 per encoder for phb_decode_seeds / phb_query_encoded: kind,
+    width or b, count, payload byte, highs byte, highs_nbits, samples byte,
+    nsamples, relative to a blob holding the encoder blocks back to back."""
     rows = []
     at = 0
     for e in encs:
@@ -172,9 +173,20 @@ def _col_info(encs, geo_at0=None) -> np.ndarray:
             rows.append([0, e.width, e.count, at + 10, 0, 0, 0, 0])
         else:
             pay = at + 22 + 8 * len(e.samples)
-            rows.append([1, e.b, e.count, pay, pay + len(e.lows), e.highs_nbits, 0, 0])
+            rows.append([1, e.b, e.count, pay, pay + len(e.lows), e.highs_nbits, at + 22,
+                         len(e.samples)])
         at += len(e.block())
     return np.ascontiguousarray(np.array(rows, dtype=np.int64).reshape(-1, 8))
+
+
+def _device_blocks(encs):
+    """(device blob of the encoder blocks, device col_info) for phb_query_encoded."""
+    dev = _native.require_device()
+    blob = b"".join(e.block() for e in encs)
+    # zero tail: the kernel reads whole aligned u64 words past the last field
+    d_blob = torch.frombuffer(bytearray(blob + b"\0" * 32), dtype=torch.uint8).to(dev)
+    info = torch.from_numpy(_col_info(encs)).to(dev)
+    return d_blob, info
 
 
 def _decode(encs, nparts: int, bcount: int, mono: bool) -> torch.Tensor:
@@ -199,6 +211,7 @@ class InterleavedSeeds:
     compact_prefix: int
     _section: bytes | None = field(default=None, repr=False)
     _device: torch.Tensor | None = field(default=None, repr=False)
+    _encoded: tuple | None = field(default=None, repr=False)
 
     @classmethod
     def build(cls, seed_matrix: np.ndarray, compact_prefix: int) -> "InterleavedSeeds":
@@ -218,6 +231,13 @@ class InterleavedSeeds:
         if self._device is None:
             self._device = _decode(self.encoders, self.num_partitions, self.bucket_count, False)
         return self._device
+
+    def device_encoded(self):
+        """(section blob, col_info, num encoders, mono) on the device, cached."""
+        if self._encoded is None:
+            blob, info = _device_blocks(self.encoders)
+            self._encoded = (blob, info, len(self.encoders), 0)
+        return self._encoded
 
     def decode_matrix(self) -> np.ndarray:
         if not self.encoders:
@@ -240,6 +260,7 @@ class MonoSeeds:
     bucket_count: int
     _section: bytes | None = field(default=None, repr=False)
     _device: torch.Tensor | None = field(default=None, repr=False)
+    _encoded: tuple | None = field(default=None, repr=False)
 
     @classmethod
     def build(cls, seed_matrix: np.ndarray, rice: bool) -> "MonoSeeds":
@@ -260,6 +281,12 @@ class MonoSeeds:
         if self._device is None:
             self._device = _decode([self.encoder], self.num_partitions, self.bucket_count, True)
         return self._device
+
+    def device_encoded(self):
+        if self._encoded is None:
+            blob, info = _device_blocks([self.encoder])
+            self._encoded = (blob, info, 1, 1)
+        return self._encoded
 
     def decode_matrix(self) -> np.ndarray:
         return self.device_matrix().t().contiguous().cpu().numpy().view(np.uint64)

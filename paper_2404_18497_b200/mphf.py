@@ -246,7 +246,7 @@ class Mphf:
         return f"mixed:{t}"
 
     # ---- query ----------------------------------------------------------
-    def _device_state(self):
+    def _device_state(self, matrix: bool = True):
         dev = _native.require_device()
         if self._dev is not None:
             return self._dev_key_off, self._dev_entries, self._dev.seeds
@@ -258,7 +258,8 @@ class Mphf:
             self._dev_key_off = key_off
         if self._dev_entries is None:
             self._dev_entries = device_table(self.table, dev)
-        return self._dev_key_off, self._dev_entries, self.seeds.device_matrix()
+        return (self._dev_key_off, self._dev_entries,
+                self.seeds.device_matrix() if matrix else None)
 
     @property
     def num_partitions(self) -> int:
@@ -276,6 +277,23 @@ class Mphf:
                      dk.n, self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n,
                      self.num_partitions, P(key_off), P(entries), self.bcount, P(seeds),
                      1, self.num_partitions, P(out), _native.stream())
+        return out
+
+    def query_encoded_device(self, keys) -> torch.Tensor:
+        """Batched device query that reads the seeds straight from the encoded
+        section (CompactVector.get / RiceVector.get with sampled select,
+        encoders.py:89-99, :224-230) instead of a decoded seed matrix."""
+        dev = _native.require_device()
+        key_off, entries, _ = self._device_state(matrix=False)
+        blob, info, num_enc, mono = self.seeds.device_encoded()
+        dk = keys if isinstance(keys, DeviceKeys) else to_device(keys, dev)
+        out = torch.empty(dk.n, dtype=torch.int64, device=dev)
+        P = _native.ptr
+        _native.call("phb_query_encoded", None if dk.is_u64 else P(dk.buf),
+                     None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
+                     dk.n, self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n, self.num_partitions,
+                     P(key_off), P(entries), self.bcount, P(blob), P(info), num_enc, mono,
+                     P(out), _native.stream())
         return out
 
     def query_many(self, keys) -> np.ndarray:

@@ -1,0 +1,84 @@
+"""K7e: queries answered straight from the encoded seed section (no decoded
+matrix) equal the reference's queries (golden) and the matrix-based kernel,
+for every preset, including Rice columns whose select spans many samples."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def phb():
+    import paper_2404_18497_b200 as m
+    from paper_2404_18497_b200 import _native
+
+    _native.require_device()
+    return m
+
+
+def test_encoded_query_matches_reference_goldens(golden, meta, phb):
+    """Structures deserialized from the reference's own bytes, queried from
+    the encoded section, give the reference's query outputs."""
+    from paper_2404_18497_b200 import KeyCorpus, Mphf
+
+    checked = 0
+    for key, m in meta.items():
+        if not key.startswith("e2e_"):
+            continue
+        name = key[4:]
+        if f"e2e_{name}_query" not in golden.files:
+            continue
+        corpus = KeyCorpus(golden[f"e2e_{name}_buf"], golden[f"e2e_{name}_off"])
+        want = golden[f"e2e_{name}_query"]
+        for enc in m["bytes"]:
+            f = Mphf.deserialize(golden[f"e2e_{name}_{enc}"].tobytes())
+            got = f.query_encoded_device(corpus).cpu().numpy()
+            assert np.array_equal(got[: len(want)], want), (name, enc)
+            checked += 1
+    assert checked > 0
+
+
+@pytest.mark.parametrize("enc", ["ic-c", "ic-r", "mixed:40", "mono-r", "mono-c"])
+def test_encoded_query_equals_matrix_query(phb, enc):
+    """P = 100 gives 3000 partitions, so every interleaved Rice column has
+    more than one select sample (one per 1024 ones)."""
+    rng = np.random.default_rng(11)
+    keys = np.unique(rng.integers(0, 2**64, size=300_000, dtype=np.uint64))
+    cfg = phb.BuildConfig(lambda_=5.0, partition_size=100.0, encoder=enc)
+    f = phb.build(keys, cfg)
+    assert f.num_partitions > 2048
+    dk = torch.from_numpy(keys.view(np.int64)).cuda()
+    a = f.query_device(dk)
+    b = f.query_encoded_device(dk)
+    assert torch.equal(a, b), enc
+    assert f.verify_device(b)
+    # the same through a deserialized copy (section uploaded from host bytes)
+    g = phb.Mphf.deserialize(f.serialize())
+    assert torch.equal(g.query_encoded_device(dk), a), enc
+
+
+def test_encoded_query_string_keys(phb):
+    from paper_2404_18497_b200 import gen_keys
+
+    corpus = gen_keys(50_000, 3)
+    f = phb.build(corpus, phb.BuildConfig(lambda_=8.0, partition_size=500.0, encoder="ic-r"))
+    out = f.query_encoded_device(corpus)
+    assert np.array_equal(out.cpu().numpy(), f.query_many(corpus))
+    assert f.verify_device(out)
+
+
+def test_encoded_query_c2_scale(phb):
+    """100M keys of the bench workload (C2, IC-C): encoded-section queries are
+    a bijection and agree with the matrix kernel on a sample."""
+    from paper_2404_18497_b200.keygen import DeviceKeys, synth_u64_device
+
+    n = 100_000_000
+    keys = synth_u64_device(n, 0)
+    f = phb.build(DeviceKeys(n, keys64=keys),
+                  phb.BuildConfig(lambda_=9.0, partition_size=2500.0, encoder="ic-c"))
+    out = f.query_encoded_device(DeviceKeys(n, keys64=keys))
+    assert f.verify_device(out)
+    sample = keys[::997].contiguous()
+    assert torch.equal(out[::997], f.query_device(DeviceKeys(sample.numel(), keys64=sample)))
