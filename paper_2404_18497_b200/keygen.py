@@ -93,6 +93,65 @@ def _as_u64_tensor(t: torch.Tensor) -> torch.Tensor:
     raise TypeError(f"64-bit key arrays must be uint64/int64, got {t.dtype}")
 
 
+# ---- host ingestion: pageable host arrays reach the device through pinned
+# staging buffers, with the host-side copy (threaded) of chunk i+1 overlapped
+# with the DMA of chunk i. torch's pageable .to(device) runs at ~11 GB/s on
+# the B200 boxes (800 MB in 71 ms); staged, the copy approaches the PCIe rate.
+_STAGE_BYTES = 64 << 20
+_STAGE_SLOTS = 3
+_stage = {"bufs": None, "events": None, "pool": None}
+
+
+def _stage_init():
+    if _stage["bufs"] is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+
+        _stage["bufs"] = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True)
+                          for _ in range(_STAGE_SLOTS)]
+        _stage["events"] = [None] * _STAGE_SLOTS
+        _stage["pool"] = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)))
+    return _stage
+
+
+def staged_h2d(host: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Copy a C-contiguous host array to a new uint8 device tensor (its bytes)."""
+    src = np.ascontiguousarray(host).reshape(-1).view(np.uint8)
+    nbytes = src.size
+    out = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    if nbytes == 0:
+        return out[:0]
+    st = _stage_init()
+    pool = st["pool"]
+    workers = pool._max_workers
+    stream = torch.cuda.current_stream(device)
+    for k, a in enumerate(range(0, nbytes, _STAGE_BYTES)):
+        b = min(a + _STAGE_BYTES, nbytes)
+        slot = k % _STAGE_SLOTS
+        ev = st["events"][slot]
+        if ev is not None:
+            ev.synchronize()  # the DMA that last read this staging buffer is done
+        dst = st["bufs"][slot].numpy()[: b - a]
+        step = -(-(b - a) // workers)
+        futs = [pool.submit(np.copyto, dst[o: o + step], src[a + o: a + o + step])
+                for o in range(0, b - a, step)]
+        for fu in futs:
+            fu.result()
+        out[a:b].copy_(st["bufs"][slot][: b - a], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        st["events"][slot] = ev
+    return out
+
+
+def _host_to_device_u64(t: torch.Tensor, device: torch.device) -> torch.Tensor:
+    if t.is_cuda:
+        return t.to(device)
+    if t.is_pinned():
+        return t.to(device, non_blocking=True)
+    return staged_h2d(t.numpy(), device).view(torch.int64)
+
+
 def to_device(keys, device: torch.device) -> DeviceKeys:
     """Stage keys on the device. u64 arrays -> fast path; everything else -> bytes."""
     if isinstance(keys, DeviceKeys):
@@ -100,17 +159,18 @@ def to_device(keys, device: torch.device) -> DeviceKeys:
     if isinstance(keys, torch.Tensor):
         t = _as_u64_tensor(keys.reshape(-1))
         moved = 0 if t.is_cuda else t.numel() * 8
-        return DeviceKeys(int(t.numel()), keys64=t.to(device, non_blocking=True), h2d_bytes=moved)
+        return DeviceKeys(int(t.numel()), keys64=_host_to_device_u64(t, device), h2d_bytes=moved)
     if isinstance(keys, np.ndarray):
         if keys.dtype not in (np.uint64, np.int64):
             raise TypeError(f"64-bit key arrays must be uint64/int64, got {keys.dtype}")
-        host = torch.from_numpy(np.ascontiguousarray(keys).view(np.int64))
-        return DeviceKeys(len(keys), keys64=host.to(device, non_blocking=True),
-                          h2d_bytes=int(host.numel() * 8))
+        host = np.ascontiguousarray(keys).reshape(-1)
+        return DeviceKeys(len(host), keys64=staged_h2d(host, device).view(torch.int64),
+                          h2d_bytes=int(host.nbytes))
     corpus = as_corpus(keys)
-    buf = torch.from_numpy(corpus.buf) if corpus.buf.size else torch.zeros(8, dtype=torch.uint8)
-    off = torch.from_numpy(np.ascontiguousarray(corpus.offsets, dtype=np.int64))
-    return DeviceKeys(len(corpus), buf=buf.to(device), offsets=off.to(device),
+    buf = corpus.buf if corpus.buf.size else np.zeros(8, dtype=np.uint8)
+    off = np.ascontiguousarray(corpus.offsets, dtype=np.int64)
+    return DeviceKeys(len(corpus), buf=staged_h2d(buf, device),
+                      offsets=staged_h2d(off, device).view(torch.int64),
                       h2d_bytes=int(corpus.buf.nbytes + corpus.offsets.nbytes))
 
 
