@@ -394,6 +394,8 @@ def build(keys, config: BuildConfig | None = None) -> Mphf:
     (host or CUDA; 64-bit keys hash as their 8-byte little-endian string).
     """
     config = config or BuildConfig()
+    if hasattr(keys, "__len__") and len(keys) == 0:  # host-side, like the reference (mphf.py:245)
+        raise InvalidConfig("need at least one key")
     dev = _native.require_device()
     t0 = time.perf_counter()
     dk = to_device(keys, dev)

@@ -59,6 +59,16 @@ def test_no_cpu_fallback():
 
 # ---- host config logic vs the reference's frozen values (pkg/tests) ----
 
+def test_empty_input_rejected_before_the_device():
+    """build([]) raises InvalidConfig like the reference (mphf.py:243-245,
+    test_mphf.py:139-144), from host logic alone."""
+    import paper_2404_18497_b200 as phb
+
+    for empty in ([], np.zeros(0, np.uint64), phb.KeyCorpus.from_keys([])):
+        with pytest.raises(phb.InvalidConfig):
+            phb.build(empty, phb.BuildConfig())
+
+
 def test_build_config_validation():
     from paper_2404_18497_b200 import BuildConfig, InvalidConfig
     from paper_2404_18497_b200.builder import parse_encoder
