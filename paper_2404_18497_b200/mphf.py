@@ -86,6 +86,10 @@ class DeviceBuild:
     total_bytes: int
     seed_section: int
     trials_total: int
+    # instrumented builds only (BuildEngine.run(..., instrument=True)):
+    trials: torch.Tensor | None = None        # int64 column-major [B][nparts] per-bucket trials
+    part_trials: torch.Tensor | None = None   # int64 [nparts]
+    bucket_sizes: torch.Tensor | None = None  # int64 [nparts * B]: keys per (partition, bucket)
 
 
 class BuildEngine:
@@ -103,8 +107,11 @@ class BuildEngine:
         self._summary = np.zeros(8, np.int64)
         self.last_launches = 0
 
-    def run(self, dk: DeviceKeys, seed: int) -> DeviceBuild | tuple[int, int]:
-        """One attempt. Returns DeviceBuild, or (first_bad, code) on failure."""
+    def run(self, dk: DeviceKeys, seed: int,
+            instrument: bool = False) -> DeviceBuild | tuple[int, int]:
+        """One attempt. Returns DeviceBuild, or (first_bad, code) on failure.
+        instrument: also keep per-bucket trials, per-partition trials and the
+        (partition, bucket) key counts (analysis.measure_work)."""
         cfg, dev, B = self.config, self.device, self.bcount
         n = dk.n
         nparts = num_partitions_for(n, cfg.partition_size)
@@ -134,6 +141,12 @@ class BuildEngine:
         _native.check(L.phb_scatter(buf, offs, k64, n, seed, nparts, P(self.entries), B,
                                     P(key_off), P(counts), P(lo), P(bid), st), "phb_scatter")
         seeds = torch.zeros(B * nparts, dtype=torch.int64, device=dev)
+        trials = torch.zeros(B * nparts, dtype=torch.int64, device=dev) if instrument else None
+        sizes = None
+        if instrument:  # keys per (partition, bucket): analysis only, torch is plumbing here
+            part = torch.repeat_interleave(
+                torch.arange(nparts, device=dev), key_off[1:] - key_off[:-1], output_size=n)
+            sizes = torch.bincount(part * B + (bid.long() & 0xFFFF) - 1, minlength=nparts * B)
         part_trials = torch.empty(nparts, dtype=torch.int64, device=dev)
         status = torch.empty(nparts, dtype=torch.uint8, device=dev)
         glo = torch.empty(n, dtype=torch.int64, device=dev)
@@ -141,7 +154,8 @@ class BuildEngine:
         ev.synchronize()
         m_max = int(self._pinned[1])
         _native.check(L.phb_search(P(lo), P(bid), P(key_off), 0, nparts, 0, B, cfg.seed_cap,
-                                   cfg.tie_desc, m_max, P(seeds), 1, nparts, None,
+                                   cfg.tie_desc, m_max, P(seeds), 1, nparts,
+                                   P(trials) if instrument else None,
                                    P(part_trials), P(status), P(glo), P(queue), st),
                       "phb_search")
         ws = torch.empty(int(L.phb_encode_workspace_bytes(nparts, B, self.mono)),
@@ -159,7 +173,8 @@ class BuildEngine:
                                          nparts, P(stats), P(ws), P(blob), blob.numel(), st),
                       "phb_encode_write")
         return DeviceBuild(n, nparts, B, seed, key_off, deltas, seeds, blob, total,
-                           int(summ[1]), int(summ[2]))
+                           int(summ[1]), int(summ[2]), trials,
+                           part_trials if instrument else None, sizes)
 
 
 class Mphf:
