@@ -78,7 +78,8 @@ class RiceVector:
     def _highs_words(self) -> np.ndarray:
         if self._words is None:
             nw = (self.highs_nbits + 63) >> 6
-            self._words = np.frombuffer(self.highs.ljust(nw * 8, b"\0"), "<u8").astype(np.uint64)
+            self._words = np.frombuffer(bytes(self.highs).ljust(nw * 8, b"\0"),
+                                        "<u8").astype(np.uint64)
         return self._words
 
     def select1(self, k: int) -> int:
@@ -140,7 +141,7 @@ def _parse_encoder(data: bytes, at: int) -> tuple[Encoder, int, tuple]:
         nbytes = (count * param + 7) // 8
         if at + nbytes > len(data):
             raise ValueError("truncated compact payload")
-        enc = CompactVector(param, count, bytes(data[at: at + nbytes]))
+        enc = CompactVector(param, count, memoryview(data)[at: at + nbytes])
         return enc, at + nbytes, (0, param, count, at, 0, 0)
     if kind != KIND_RICE:
         raise ValueError(f"unknown encoder kind {kind}")
@@ -156,8 +157,8 @@ def _parse_encoder(data: bytes, at: int) -> tuple[Encoder, int, tuple]:
     high_bytes = (highs_nbits + 7) // 8
     if at + low_bytes + high_bytes > len(data):
         raise ValueError("truncated rice payload")
-    lows = bytes(data[at: at + low_bytes])
-    highs = bytes(data[at + low_bytes: at + low_bytes + high_bytes])
+    lows = memoryview(data)[at: at + low_bytes]  # zero-copy views of the parsed bytes
+    highs = memoryview(data)[at + low_bytes: at + low_bytes + high_bytes]
     geo = (1, param, count, at, at + low_bytes, highs_nbits)
     return RiceVector(param, count, lows, highs, highs_nbits, samples), at + low_bytes + high_bytes, geo
 
@@ -175,29 +176,51 @@ def _col_info(encs, geo_at0=None) -> np.ndarray:
             pay = at + 22 + 8 * len(e.samples)
             rows.append([1, e.b, e.count, pay, pay + len(e.lows), e.highs_nbits, at + 22,
                          len(e.samples)])
-        at += len(e.block())
+        at += _block_len(e)
     return np.ascontiguousarray(np.array(rows, dtype=np.int64).reshape(-1, 8))
 
 
-def _device_blocks(encs):
-    """(device blob of the encoder blocks, device col_info) for phb_query_encoded."""
-    dev = _native.require_device()
-    blob = b"".join(e.block() for e in encs)
-    # zero tail: the kernel reads whole aligned u64 words past the last field
-    d_blob = torch.frombuffer(bytearray(blob + b"\0" * 32), dtype=torch.uint8).to(dev)
-    info = torch.from_numpy(_col_info(encs)).to(dev)
-    return d_blob, info
+def _block_len(e) -> int:
+    if isinstance(e, CompactVector):
+        return 10 + len(e.data)
+    return 22 + 8 * len(e.samples) + len(e.lows) + len(e.highs)
 
 
-def _decode(encs, nparts: int, bcount: int, mono: bool) -> torch.Tensor:
+def _blocks_bytes(store) -> memoryview:
+    """The encoder blocks back to back = the serialized section minus its u32 count."""
+    return memoryview(store.section())[4:]
+
+
+def _device_blocks(store):
+    """Device copy of the encoder blocks (8-byte aligned, zero tail: the
+    kernels read whole aligned u64 words past the last field) + col_info.
+    A freshly built structure copies them from its device body; a loaded one
+    uploads them once through the pinned staging path. Cached on the store."""
+    if store._dev_blocks is None:
+        from .keygen import staged_h2d
+
+        dev = _native.require_device()
+        encs = store.encoders if isinstance(store, InterleavedSeeds) else [store.encoder]
+        src = store._dev_source
+        if src is not None:  # (device body, first block byte, end byte)
+            body, a, b = src
+            d_blob = torch.zeros(b - a + 32, dtype=torch.uint8, device=body.device)
+            d_blob[: b - a].copy_(body[a:b])
+        else:
+            blocks = np.frombuffer(_blocks_bytes(store), dtype=np.uint8)
+            d_blob = staged_h2d(blocks, dev, pad=32)
+        info = _col_info(encs)
+        store._dev_blocks = (d_blob, torch.from_numpy(info).to(dev), info)
+    return store._dev_blocks
+
+
+def _decode(store, nparts: int, bcount: int, mono: bool) -> torch.Tensor:
     """Device decode -> column-major u64 matrix [bcount][nparts] (torch int64 view)."""
     dev = _native.require_device()
-    blob = b"".join(e.block() for e in encs)
-    d_blob = torch.frombuffer(bytearray(blob + b"\0" * 16), dtype=torch.uint8).to(dev)
-    info = _col_info(encs)
+    d_blob, _, hinfo = _device_blocks(store)
     out = torch.zeros(bcount * nparts, dtype=torch.int64, device=dev)
-    _native.call("phb_decode_seeds", _native.ptr(d_blob), len(encs),
-                 info.ctypes.data_as(__import__("ctypes").c_void_p), nparts, bcount, int(mono),
+    _native.call("phb_decode_seeds", _native.ptr(d_blob), len(hinfo),
+                 hinfo.ctypes.data_as(__import__("ctypes").c_void_p), nparts, bcount, int(mono),
                  _native.ptr(out), _native.stream())
     return out.view(bcount, nparts)
 
@@ -212,6 +235,8 @@ class InterleavedSeeds:
     _section: bytes | None = field(default=None, repr=False)
     _device: torch.Tensor | None = field(default=None, repr=False)
     _encoded: tuple | None = field(default=None, repr=False)
+    _dev_blocks: tuple | None = field(default=None, repr=False)
+    _dev_source: tuple | None = field(default=None, repr=False)
 
     @classmethod
     def build(cls, seed_matrix: np.ndarray, compact_prefix: int) -> "InterleavedSeeds":
@@ -229,13 +254,13 @@ class InterleavedSeeds:
     def device_matrix(self) -> torch.Tensor:
         """Column-major [B][nparts] u64 seeds on the device (cached)."""
         if self._device is None:
-            self._device = _decode(self.encoders, self.num_partitions, self.bucket_count, False)
+            self._device = _decode(self, self.num_partitions, self.bucket_count, False)
         return self._device
 
     def device_encoded(self):
         """(section blob, col_info, num encoders, mono) on the device, cached."""
         if self._encoded is None:
-            blob, info = _device_blocks(self.encoders)
+            blob, info, _ = _device_blocks(self)
             self._encoded = (blob, info, len(self.encoders), 0)
         return self._encoded
 
@@ -261,6 +286,8 @@ class MonoSeeds:
     _section: bytes | None = field(default=None, repr=False)
     _device: torch.Tensor | None = field(default=None, repr=False)
     _encoded: tuple | None = field(default=None, repr=False)
+    _dev_blocks: tuple | None = field(default=None, repr=False)
+    _dev_source: tuple | None = field(default=None, repr=False)
 
     @classmethod
     def build(cls, seed_matrix: np.ndarray, rice: bool) -> "MonoSeeds":
@@ -279,12 +306,12 @@ class MonoSeeds:
 
     def device_matrix(self) -> torch.Tensor:
         if self._device is None:
-            self._device = _decode([self.encoder], self.num_partitions, self.bucket_count, True)
+            self._device = _decode(self, self.num_partitions, self.bucket_count, True)
         return self._device
 
     def device_encoded(self):
         if self._encoded is None:
-            blob, info = _device_blocks([self.encoder])
+            blob, info, _ = _device_blocks(self)
             self._encoded = (blob, info, 1, 1)
         return self._encoded
 
@@ -309,7 +336,7 @@ def parse_section(data: bytes, at: int, num_partitions: int, bcount: int):
     for _ in range(num_enc):
         enc, at, _geo = _parse_encoder(data, at)
         encs.append(enc)
-    section = bytes(data[start:at])
+    section = memoryview(data)[start:at]
     if num_enc == 1 and bcount > 1:
         if encs[0].count != num_partitions * bcount:
             raise ValueError("mono encoder count does not match layout")

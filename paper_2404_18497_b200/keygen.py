@@ -114,13 +114,16 @@ def _stage_init():
     return _stage
 
 
-def staged_h2d(host: np.ndarray, device: torch.device) -> torch.Tensor:
-    """Copy a C-contiguous host array to a new uint8 device tensor (its bytes)."""
+def staged_h2d(host: np.ndarray, device: torch.device, pad: int = 0) -> torch.Tensor:
+    """Copy a C-contiguous host array to a new uint8 device tensor (its bytes),
+    followed by `pad` zero bytes."""
     src = np.ascontiguousarray(host).reshape(-1).view(np.uint8)
     nbytes = src.size
-    out = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    out = torch.empty(max(nbytes + pad, 1), dtype=torch.uint8, device=device)
+    if pad:
+        out[nbytes:].zero_()
     if nbytes == 0:
-        return out[:0]
+        return out[: nbytes + pad]
     st = _stage_init()
     pool = st["pool"]
     workers = pool._max_workers
@@ -141,7 +144,7 @@ def staged_h2d(host: np.ndarray, device: torch.device) -> torch.Tensor:
         ev = torch.cuda.Event()
         ev.record(stream)
         st["events"][slot] = ev
-    return out
+    return out if pad else out[:nbytes]
 
 
 def _host_to_device_u64(t: torch.Tensor, device: torch.device) -> torch.Tensor:

@@ -253,6 +253,8 @@ class Mphf:
             store, _ = parse_section(memoryview(self._body), db.seed_section, db.nparts,
                                      db.bcount)
             store._device = db.seeds.view(db.bcount, db.nparts)
+            # encoded blocks for query_encoded_device come from the device body
+            store._dev_source = (db.blob, db.seed_section + 4, db.total_bytes)
             self._seeds = store
         return self._seeds
 
@@ -387,7 +389,8 @@ class Mphf:
         if version != VERSION:
             raise FormatError(f"unsupported version {version}")
         (stored,) = struct.unpack_from("<Q", data, len(data) - 8)
-        if _checksum(data[:-8]) != stored:
+        body = memoryview(data)[:-8]  # zero-copy: checksum, parse and body share the bytes
+        if _checksum(body) != stored:
             raise FormatError("checksum mismatch")
         try:
             n, nparts, lambda_, psize, kind_code, epsilon, global_seed, width = struct.unpack_from(
@@ -411,7 +414,7 @@ class Mphf:
         layout = PartitionLayout(n=n, num_partitions=nparts, deltas=deltas)
         table = tabulate(AssignmentSpec(KINDS[kind_code], epsilon))
         f = cls(global_seed, layout, table, bcount, store, lambda_, psize)
-        f._body = data[:-8]
+        f._body = body
         return f
 
     @classmethod
