@@ -23,7 +23,7 @@ constexpr uint64_t MM_F1 = 0xFF51AFD7ED558CCDull;
 constexpr uint64_t MM_F2 = 0xC4CEB9FE1A85EC53ull;
 constexpr int GRID = 2048;  // assignment.py:26
 
-__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+__host__ __device__ constexpr uint64_t mix64(uint64_t z) {
   z ^= z >> 30;
   z *= MIX1;
   z ^= z >> 27;

@@ -42,6 +42,23 @@ namespace phb {
 #ifndef PHB_MINB
 #define PHB_MINB 8
 #endif
+// The per-seed hash mix64(s ^ POSITION_SALT) (_kernels.py:330) for the first
+// GTAB_N seeds, computed at compile time: one L1-resident load per batch
+// lane instead of a 64-bit mix (seeds at C2 stay below ~3,500).
+constexpr int GTAB_N = 4096;
+struct SeedHashTable {
+  uint64_t v[GTAB_N];
+};
+constexpr SeedHashTable make_seed_hashes() {
+  SeedHashTable t{};
+  for (int s = 0; s < GTAB_N; ++s) t.v[s] = mix64((uint64_t)s ^ POSITION_SALT);
+  return t;
+}
+__device__ const SeedHashTable g_seed_hash = make_seed_hashes();
+
+__device__ __forceinline__ uint64_t seed_hash(int64_t s) {
+  return s < GTAB_N ? __ldg(&g_seed_hash.v[s]) : mix64((uint64_t)s ^ POSITION_SALT);
+}
 
 constexpr int SH = 256;     // size classes of the counting-sort bucket order
 constexpr int PMAX = 256;   // bucket sizes whose base positions are staged in smem
@@ -257,7 +274,7 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
     STAT(5, (k + 31) / 32);
     const int64_t pbase = s * (int64_t)m;
     if (s > 0 && pbase > cap) return {0, trials, 2};  // _kernels.py:324-328
-    const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
+    const uint64_t g = seed_hash(s);
     bool coll = false;
     uint32_t cmask = 0;  // per-round collision flags (s = 0 duplicate check)
     if (k <= 32) {
@@ -379,7 +396,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     }
     STAT(G == 1 ? 0 : (G == 2 ? 1 : 2), 1);
     const int64_t s = s_next + grp;
-    const uint64_t g = mix64((uint64_t)s ^ POSITION_SALT);
+    const uint64_t g = seed_hash(s);
     const uint32_t p = position(key, g, m);
     const uint32_t tag = act ? (((uint32_t)grp << 16) | p) : (0x80000000u | (uint32_t)lane);
     // every lane must execute the vote (no short-circuit around it)
@@ -396,8 +413,9 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     // mask table (dmax = m - 1) or, near the seed cap, computed here
     uint32_t acc[WPL];
     if (G > 1) {
+      // a self-colliding group (rare) is masked out after the sweep instead
 #pragma unroll
-      for (int t = 0; t < WPL; ++t) acc[t] = gcoll ? FULL : smem[dmask + wb + t];
+      for (int t = 0; t < WPL; ++t) acc[t] = smem[dmask + wb + t];
     } else if (dmax == (int64_t)m - 1) {
 #pragma unroll
       for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : smem[dmask + wb + t];
@@ -437,7 +455,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     uint32_t sat = FULL;
 #pragma unroll
     for (int t = 0; t < WPL; ++t) sat &= acc[t];
-    const bool hv = sat != FULL;
+    const bool hv = sat != FULL && !(G > 1 && gcoll);
     const uint32_t fball = __ballot_sync(FULL, hv);
     int64_t myd = -1;
     if (hv) {
