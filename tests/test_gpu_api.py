@@ -242,3 +242,22 @@ def test_hundred_million_properties(phb):
     h = phb.Mphf.deserialize(f.serialize())
     sample = keys[:5_000_000]
     assert torch.equal(h.query_device(sample), f.query_device(sample))
+
+
+def test_staged_ingestion_equals_device_keys(phb):
+    """Pageable host keys (numpy, strided numpy, CPU tensor; 80 MB = two
+    staging chunks) reach the device byte-identical to CUDA-resident keys."""
+    from paper_2404_18497_b200.keygen import staged_h2d, synth_u64_device
+
+    n = 10_000_001  # odd, > one 64 MB staging chunk
+    dev_keys = synth_u64_device(n, 77)
+    host = dev_keys.cpu().numpy()
+    for src in (host, host.view(np.uint64), np.repeat(host, 2)[::2], torch.from_numpy(host)):
+        got = staged_h2d(np.asarray(src), dev_keys.device).view(torch.int64)
+        assert torch.equal(got, dev_keys)
+    cfg = phb.BuildConfig(lambda_=6.0, partition_size=2500.0, encoder="ic-r")
+    a = phb.build(dev_keys, cfg).serialize()
+    b = phb.build(host.view(np.uint64), cfg).serialize()
+    assert a == b
+    padded = staged_h2d(np.arange(5, dtype=np.uint8), dev_keys.device, pad=11)
+    assert padded.numel() == 16 and padded[5:].sum().item() == 0
