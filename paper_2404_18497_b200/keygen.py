@@ -13,6 +13,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Iterable, Iterator
 
+import threading
+
 import numpy as np
 import torch
 
@@ -100,6 +102,7 @@ def _as_u64_tensor(t: torch.Tensor) -> torch.Tensor:
 _STAGE_BYTES = 64 << 20
 _STAGE_SLOTS = 3
 _stage = {"bufs": None, "events": None, "pool": None}
+_stage_lock = threading.Lock()  # the staging buffers are shared: one copy at a time
 
 
 def _stage_init():
@@ -124,6 +127,12 @@ def staged_h2d(host: np.ndarray, device: torch.device, pad: int = 0) -> torch.Te
         out[nbytes:].zero_()
     if nbytes == 0:
         return out[: nbytes + pad]
+    with _stage_lock:
+        _staged_copy(src, out, nbytes, device)
+    return out if pad else out[:nbytes]
+
+
+def _staged_copy(src: np.ndarray, out: torch.Tensor, nbytes: int, device) -> None:
     st = _stage_init()
     pool = st["pool"]
     workers = pool._max_workers
@@ -144,7 +153,6 @@ def staged_h2d(host: np.ndarray, device: torch.device, pad: int = 0) -> torch.Te
         ev = torch.cuda.Event()
         ev.record(stream)
         st["events"][slot] = ev
-    return out if pad else out[:nbytes]
 
 
 def _host_to_device_u64(t: torch.Tensor, device: torch.device) -> torch.Tensor:
