@@ -85,52 +85,61 @@ __device__ __forceinline__ Hash128 murmur3_u64(uint64_t key, uint64_t seed) {
   return mm_final(h1, seed, 8ull);
 }
 
-// Variable-length path over a byte buffer (_kernels.py:89-146).
-// Loads are byte-granular through 8-byte assembled reads; buf may be
-// arbitrarily aligned.
-__device__ __forceinline__ uint64_t load_le(const uint8_t* __restrict__ p, int nbytes) {
-  uint64_t v = 0;
-#pragma unroll 8
-  for (int b = 0; b < nbytes; ++b) v |= (uint64_t)__ldg(p + b) << (8 * b);
-  return v;
+// Little-endian bytes [p, p + nbytes), 1 <= nbytes <= 8, from the aligned
+// 8-byte words that contain them: the second word is read only when the
+// bytes spill into it, so no word without a key byte is touched.
+__device__ __forceinline__ uint64_t load_le_words(const uint8_t* __restrict__ p, int nbytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+  const int sh = int(a & 7);
+  uint64_t v = __ldg(w) >> (8 * sh);
+  if (sh + nbytes > 8) v |= __ldg(w + 1) << (64 - 8 * sh);
+  return nbytes >= 8 ? v : (v & ((1ull << (8 * nbytes)) - 1));
 }
 
-__device__ __forceinline__ uint64_t load8_le(const uint8_t* __restrict__ p) {
-  // assemble from the two aligned 8-byte words that cover p..p+7
-  uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  uintptr_t base = a & ~uintptr_t(7);
-  int sh = int(a - base);
-  const uint64_t* w = reinterpret_cast<const uint64_t*>(base);
-  uint64_t lo = __ldg(w);
-  if (sh == 0) return lo;
-  uint64_t hi = __ldg(w + 1);
-  return (lo >> (8 * sh)) | (hi << (64 - 8 * sh));
-}
-
+// Variable-length path over a byte buffer (_kernels.py:89-146); the key may
+// be arbitrarily aligned: bytes are assembled from aligned 8-byte words.
 __device__ __forceinline__ Hash128 murmur3_bytes(const uint8_t* __restrict__ key, int64_t len,
                                                  uint64_t seed) {
   uint64_t h1 = seed, h2 = seed;
-  int64_t nblocks = len >> 4;
-  for (int64_t blk = 0; blk < nblocks; ++blk) {
-    uint64_t k1 = load8_le(key + blk * 16);
-    uint64_t k2 = load8_le(key + blk * 16 + 8);
-    h1 ^= mm_k1(k1);
-    h1 = rotl64(h1, 27);
-    h1 += h2;
-    h1 = h1 * 5 + 0x52DCE729ull;
-    h2 ^= mm_k2(k2);
-    h2 = rotl64(h2, 31);
-    h2 += h1;
-    h2 = h2 * 5 + 0x38495AB5ull;
+  const int64_t nblocks = len >> 4;
+  if (nblocks > 0) {
+    // 16-byte blocks from consecutive aligned words: word i+1 of one block
+    // is word 0 of the next (one load per 8 bytes when the key is unaligned)
+    const uintptr_t a = reinterpret_cast<uintptr_t>(key);
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+    const int sh = int(a & 7) * 8;
+    uint64_t w0 = __ldg(w);
+    for (int64_t blk = 0; blk < nblocks; ++blk) {
+      uint64_t k1, k2;
+      if (sh == 0) {
+        k1 = w0;
+        k2 = __ldg(w + 2 * blk + 1);
+        if (blk + 1 < nblocks) w0 = __ldg(w + 2 * blk + 2);
+      } else {
+        const uint64_t w1 = __ldg(w + 2 * blk + 1), w2 = __ldg(w + 2 * blk + 2);
+        k1 = (w0 >> sh) | (w1 << (64 - sh));
+        k2 = (w1 >> sh) | (w2 << (64 - sh));
+        w0 = w2;
+      }
+      h1 ^= mm_k1(k1);
+      h1 = rotl64(h1, 27);
+      h1 += h2;
+      h1 = h1 * 5 + 0x52DCE729ull;
+      h2 ^= mm_k2(k2);
+      h2 = rotl64(h2, 31);
+      h2 += h1;
+      h2 = h2 * 5 + 0x38495AB5ull;
+    }
   }
   const uint8_t* tail = key + nblocks * 16;
-  int rem = int(len - nblocks * 16);
+  const int rem = int(len - nblocks * 16);
   uint64_t k1 = 0, k2 = 0;
   if (rem > 8) {
-    k1 = load8_le(tail);
-    k2 = load_le(tail + 8, rem - 8);
+    k1 = load_le_words(tail, 8);
+    k2 = load_le_words(tail + 8, rem - 8);
   } else if (rem > 0) {
-    k1 = rem == 8 ? load8_le(tail) : load_le(tail, rem);
+    k1 = load_le_words(tail, rem);
   }
   h2 ^= mm_k2(k2);
   h1 ^= mm_k1(k1);
