@@ -302,24 +302,24 @@ def run_gpu(args):
     else:  # each rank checks its shard's outputs are distinct and in range
         assert bool(((out >= 0) & (out < f.n)).all()) and out.unique().numel() == out.numel()
     torch.cuda.synchronize()
-    q0 = torch.cuda.Event(enable_timing=True)
-    q1 = torch.cuda.Event(enable_timing=True)
-    q0.record()
-    for _ in range(3):
-        out = f.query_device(qdk)
-    q1.record()
-    torch.cuda.synchronize()
-    q_ms = q0.elapsed_time(q1) / 3
+    def time_query(fn, reps=5):
+        """median of per-call device times (CUDA events around each call)"""
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = fn(qdk)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts), r
+
+    q_ms, out = time_query(f.query_device)
     # the same batched query reading the seeds from the encoded section (K7e)
-    oute = f.query_encoded_device(qdk)
+    qe_ms, oute = time_query(f.query_encoded_device)
     enc_ok = bool(torch.equal(oute, out))
-    torch.cuda.synchronize()
-    q0.record()
-    for _ in range(3):
-        oute = f.query_encoded_device(qdk)
-    q1.record()
-    torch.cuda.synchronize()
-    qe_ms = q0.elapsed_time(q1) / 3
 
     peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))

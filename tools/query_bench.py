@@ -22,3 +22,15 @@ for name, fn in (("matrix", f.query_device), ("encoded", f.query_encoded_device)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
     print(f"{enc} {name:8s} {ms:7.3f} ms  {n / ms / 1e6:8.2f} Gq/s  bijection {f.verify_device(out)}")
+g = phb.Mphf.deserialize(f.serialize())
+for name, fn in (("loaded matrix", g.query_device), ("loaded encoded", g.query_encoded_device)):
+    out = fn(dk)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        out = fn(dk)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    print(f"{enc} {name:15s} {ms:7.3f} ms  {n / ms / 1e6:8.2f} Gq/s")
