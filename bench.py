@@ -352,7 +352,8 @@ def run_gpu(args):
         "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / (1e9 / PUBLISHED_NS_PER_KEY),
         "dtype": "u64", "data": "synthetic",
-        "config": {"workload": "C2: n=100M u64 keys/GPU, lambda=9, P=2500, IC-C (fast-query)",
+        "config": {"workload": f"C2: n={n / 1e6:g}M u64 keys/GPU, lambda=9, P=2500, IC-C "
+                               "(fast-query)",
                    "n_keys_per_gpu": n, "lambda": LAMBDA, "partition_size": PSIZE,
                    "encoder": ENCODER, "global_seed": 0,
                    "l2": "inputs (800 MB keys + 1 GB grouped records) exceed the 126 MB L2",

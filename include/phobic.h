@@ -137,6 +137,36 @@ int phb_encode_write(const uint64_t* seeds, int64_t nparts, int32_t bcount, int3
                      const int64_t* layout_stats, void* workspace, uint8_t* blob,
                      size_t blob_bytes, void* stream);
 
+/* Sharded K5 (multi-GPU, one call sequence per rank; distributed.py step 7).
+ * A rank holds the seed rows [row0, row0 + nparts) of the global matrix
+ * (column-major [bcount][nparts] locally, nparts may be 0):
+ *   1. phb_encode_shard_stats: per-column max + 64 bit-population counts
+ *      of the local rows -> colstat_out (DEVICE u64[ncols][65]); the caller
+ *      reduces them over ranks (MAX of [c][0], SUM of [c][1..64]);
+ *   2. phb_encode_shard_plan: the global plan from the reduced stats (same
+ *      geometry, sizes and summary on every rank) and this rank's Rice unary
+ *      totals per column -> rice_totals_out (DEVICE u64[ncols]);
+ *   3. phb_encode_shard_write: this rank's fields at their global bit
+ *      addresses into a zeroed body; rice_base (DEVICE u64[ncols]) = the
+ *      unary totals of lower ranks; write_headers on exactly one rank.
+ * Every bit of the body is written by exactly one rank, so a byte-wise SUM
+ * over ranks (ncclAllReduce, uint8) is their OR: the single-GPU body.
+ * workspace: phb_encode_workspace_bytes(nparts, bcount, mono). */
+int phb_encode_shard_stats(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                           unsigned long long* colstat_out, void* stream);
+int phb_encode_shard_plan(const uint64_t* seeds, int64_t nparts, int64_t row0,
+                          int64_t nparts_global, int32_t bcount, int32_t mono,
+                          int32_t compact_prefix, const int64_t* layout_stats,
+                          const unsigned long long* colstat_global, void* workspace,
+                          unsigned long long* rice_totals_out, int64_t* summary_out,
+                          void* stream);
+int phb_encode_shard_write(const uint64_t* seeds, int64_t nparts, int64_t row0,
+                           int64_t nparts_global, int32_t bcount, int32_t mono,
+                           int32_t compact_prefix, const int64_t* deltas,
+                           const int64_t* layout_stats, const unsigned long long* rice_base,
+                           int32_t write_headers, void* workspace, uint8_t* blob,
+                           size_t blob_bytes, void* stream);
+
 /* Decode an encoded seed section (device copy of a serialized body) back to
  * the column-major matrix seeds[bcount][nparts] (decode_matrix,
  * encoders.py:309-311 / :337-338). col_info: HOST array of 8 int64 per

@@ -37,6 +37,9 @@ SIGNATURES = {
     "phb_encode_plan": [P, I64, I32, I32, I32, P, I64, P, P, P, P, P, P],
     "phb_encode_write": [P, I64, I32, I32, I32, P, I64, P, P, P, SZ, P],
     "phb_decode_seeds": [P, I64, P, I64, I32, I32, P, P],
+    "phb_encode_shard_stats": [P, I64, I32, I32, P, P],
+    "phb_encode_shard_plan": [P, I64, I64, I64, I32, I32, I32, P, P, P, P, P, P],
+    "phb_encode_shard_write": [P, I64, I64, I64, I32, I32, I32, P, P, P, I32, P, P, SZ, P],
     "phb_query": [P, P, P, I64, U64, I64, I64, P, P, I32, P, I64, I64, P, P],
     "phb_query_encoded": [P, P, P, I64, U64, I64, I64, P, P, I32, P, P, I32, I32, P, P],
     "phb_verify": [P, I64, I64, P, P, P],

@@ -287,6 +287,61 @@ int phb_encode_write(const uint64_t* seeds, int64_t nparts, int32_t bcount, int3
   return launch_encode_write(a, workspace, blob, blob_bytes, S(stream));
 }
 
+// ---- sharded encode (multi-GPU, distributed.py step 7)
+int phb_encode_shard_stats(const uint64_t* seeds, int64_t nparts, int32_t bcount, int32_t mono,
+                           unsigned long long* colstat_out, void* stream) {
+  if (bcount < 1 || nparts < 0 || !colstat_out) return PHB_E_ARGS;
+  EncodeArgs a = make_enc(seeds, nparts, bcount, mono, 0, nullptr, nparts, nullptr, nullptr,
+                          nullptr);
+  return launch_encode_stats(a, nullptr, colstat_out, S(stream));
+}
+
+int phb_encode_shard_plan(const uint64_t* seeds, int64_t nparts, int64_t row0,
+                          int64_t nparts_global, int32_t bcount, int32_t mono,
+                          int32_t compact_prefix, const int64_t* layout_stats,
+                          const unsigned long long* colstat_global, void* workspace,
+                          unsigned long long* rice_totals_out, int64_t* summary_out,
+                          void* stream) {
+  if (bcount < 1 || nparts < 0 || row0 < 0 || row0 + nparts > nparts_global || !layout_stats ||
+      !workspace || !colstat_global || !rice_totals_out)
+    return PHB_E_ARGS;
+  EncodeArgs a = make_enc(seeds, nparts, bcount, mono, compact_prefix, nullptr, nparts_global,
+                          layout_stats, nullptr, nullptr);
+  a.row0 = row0;
+  a.count_global = mono ? nparts_global * (int64_t)bcount : nparts_global;
+  a.colstat_in = colstat_global;
+  a.rice_totals_out = rice_totals_out;
+  EncodeSummary s;
+  int rc = launch_encode_plan(a, workspace, summary_out ? &s : nullptr, S(stream));
+  if (rc == 0 && summary_out) {
+    summary_out[0] = (int64_t)s.total_bytes;
+    summary_out[1] = (int64_t)s.seed_section;
+    summary_out[2] = 0;
+    summary_out[3] = -1;
+    summary_out[4] = 0;
+    summary_out[5] = s.delta_width;
+    summary_out[6] = s.ncols;
+    summary_out[7] = 0;
+  }
+  return rc;
+}
+
+int phb_encode_shard_write(const uint64_t* seeds, int64_t nparts, int64_t row0,
+                           int64_t nparts_global, int32_t bcount, int32_t mono,
+                           int32_t compact_prefix, const int64_t* deltas,
+                           const int64_t* layout_stats, const unsigned long long* rice_base,
+                           int32_t write_headers, void* workspace, uint8_t* blob,
+                           size_t blob_bytes, void* stream) {
+  if (bcount < 1 || nparts < 0 || !workspace || !blob || !layout_stats) return PHB_E_ARGS;
+  EncodeArgs a = make_enc(seeds, nparts, bcount, mono, compact_prefix, deltas, nparts_global,
+                          layout_stats, nullptr, nullptr);
+  a.row0 = row0;
+  a.count_global = mono ? nparts_global * (int64_t)bcount : nparts_global;
+  a.rice_base = rice_base;
+  a.write_headers = write_headers;
+  return launch_encode_write(a, workspace, blob, blob_bytes, S(stream));
+}
+
 int phb_decode_seeds(const uint8_t* blob, int64_t ncols, const int64_t* col_info, int64_t nparts,
                      int32_t bcount, int32_t mono, uint64_t* seeds, void* stream) {
   if (bcount < 1 || nparts < 1 || !col_info) return PHB_E_ARGS;

@@ -51,6 +51,7 @@ struct Cols {
   int64_t nparts;
   uint32_t B;
   int mono;
+  int64_t t_off;          // global index of this shard's value 0 in every column
   __device__ __forceinline__ int64_t ncols() const { return mono ? 1 : B; }
   __device__ __forceinline__ int64_t count() const { return mono ? nparts * (int64_t)B : nparts; }
   // value t of column c in the reference's order
@@ -120,7 +121,8 @@ __global__ void __launch_bounds__(1024) k_plan(EncodeArgs a, const unsigned long
   __shared__ unsigned long long s_trials;
   __shared__ int s_bad;
   const int ncols = a.mono ? 1 : (int)a.bcount;
-  const int64_t cnt = a.mono ? a.nparts * (int64_t)a.bcount : a.nparts;
+  const int64_t cnt = a.count_global ? a.count_global
+                                     : (a.mono ? a.nparts * (int64_t)a.bcount : a.nparts);
   if (threadIdx.x == 0) s_trials = 0, s_bad = 0x7fffffff;
   __syncthreads();
   // status / trials over partitions
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(ET) k_rice_chunks(Cols cols, int64_t nchunks_p
   if (ci.kind != 1) return;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
-  const int64_t t0 = q * ECH, t1 = min(t0 + (int64_t)ECH, (int64_t)ci.count);
+  const int64_t t0 = q * ECH, t1 = min(t0 + (int64_t)ECH, cols.count());
   unsigned long long acc = 0;
   const int b = ci.param;
   for (int64_t t = t0 + threadIdx.x; t < t1; t += ET) {
@@ -255,7 +257,8 @@ __global__ void __launch_bounds__(ET) k_rice_chunks(Cols cols, int64_t nchunks_p
 
 // R2: exclusive scan of chunk sums inside each column (thread per column).
 __global__ void k_rice_chunk_scan(int64_t ncols, int64_t nchunks_per_col,
-                                  unsigned long long* __restrict__ chunk_sum) {
+                                  unsigned long long* __restrict__ chunk_sum,
+                                  unsigned long long* __restrict__ col_total) {
   int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= ncols) return;
   unsigned long long run = 0;
@@ -264,6 +267,7 @@ __global__ void k_rice_chunk_scan(int64_t ncols, int64_t nchunks_per_col,
     chunk_sum[c * nchunks_per_col + q] = run;
     run += v;
   }
+  if (col_total) col_total[c] = run;  // this shard's unary bits (sharded encode)
 }
 
 // E3: headers, deltas and every payload bit.
@@ -306,18 +310,20 @@ __global__ void k_deltas(const int64_t* __restrict__ deltas, int64_t count,
 __global__ void __launch_bounds__(ET) k_payload(Cols cols, int64_t nchunks_per_col,
                                                 const ColInfo* __restrict__ info,
                                                 const unsigned long long* __restrict__ chunk_pre,
+                                                const unsigned long long* __restrict__ rice_base,
                                                 uint32_t* __restrict__ blob) {
   __shared__ unsigned long long sh[ET / 32];
   const int64_t c = blockIdx.x / nchunks_per_col;
   const int64_t q = blockIdx.x - c * nchunks_per_col;
   const ColInfo ci = info[c];
   const int64_t t0 = q * ECH;
-  const int64_t t1 = min(t0 + (int64_t)ECH, (int64_t)ci.count);
+  const int64_t t1 = min(t0 + (int64_t)ECH, cols.count());
   if (t0 >= t1) return;
   const int b = ci.param;
+  const uint64_t toff = (uint64_t)cols.t_off;  // global index = local + toff
   if (ci.kind == 0) {
     for (int64_t t = t0 + threadIdx.x; t < t1; t += ET)
-      put_bits(blob, ci.pay_bit + (uint64_t)t * b, cols.at(c, t), b);
+      put_bits(blob, ci.pay_bit + ((uint64_t)t + toff) * b, cols.at(c, t), b);
     return;
   }
   // Rice: thread owns EPT consecutive values so the unary scan is local
@@ -351,16 +357,18 @@ __global__ void __launch_bounds__(ET) k_payload(Cols cols, int64_t nchunks_per_c
     if (lane < ET / 32) sh[lane] = x;
   }
   __syncthreads();
-  unsigned long long run = chunk_pre[blockIdx.x] + (wid ? sh[wid - 1] : 0ull) + v - local;
+  unsigned long long run = (rice_base ? rice_base[c] : 0ull) + chunk_pre[blockIdx.x] +
+                           (wid ? sh[wid - 1] : 0ull) + v - local;
 #pragma unroll
   for (int e = 0; e < EPT; ++e) {
     int64_t t = mine0 + e;
     if (t < t1) {
+      const uint64_t tg = (uint64_t)t + toff;
       const uint64_t hv = b >= 64 ? 0ull : (vals[e] >> b);
       const uint64_t one = run + hv;  // position of this value's terminating 1
       put_bits(blob, ci.highs_bit + one, 1ull, 1);
-      if (b > 0) put_bits(blob, ci.pay_bit + (uint64_t)t * b, vals[e] & lmask, b);
-      if ((t & 1023) == 0) put_bits(blob, 8ull * ci.samples_byte + 64ull * (t >> 10), one, 64);
+      if (b > 0) put_bits(blob, ci.pay_bit + tg * b, vals[e] & lmask, b);
+      if ((tg & 1023) == 0) put_bits(blob, 8ull * ci.samples_byte + 64ull * (tg >> 10), one, 64);
       run += hv + 1;
     }
   }
@@ -411,15 +419,21 @@ int launch_encode_plan(const EncodeArgs& a, void* ws, EncodeSummary* host_sum, c
   int64_t nch = cdiv(cnt, ECH);
   if (nch < 1) nch = 1;
   WsLayout L = carve(ws, ncols, nch);
-  PHB_CUDA_TRY(cudaMemsetAsync(L.colstat, 0, (size_t)ncols * 65 * 8, st));
-  Cols cols{a.seeds, a.nparts, a.bcount, a.mono};
-  k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.colstat);
-  PHB_CUDA_TRY(cudaGetLastError());
+  Cols cols{a.seeds, a.nparts, a.bcount, a.mono, a.row0 * (a.mono ? (int64_t)a.bcount : 1)};
+  if (a.colstat_in) {  // sharded: statistics already reduced over all shards
+    PHB_CUDA_TRY(cudaMemcpyAsync(L.colstat, a.colstat_in, (size_t)ncols * 65 * 8,
+                                 cudaMemcpyDeviceToDevice, st));
+  } else {
+    PHB_CUDA_TRY(cudaMemsetAsync(L.colstat, 0, (size_t)ncols * 65 * 8, st));
+    k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.colstat);
+    PHB_CUDA_TRY(cudaGetLastError());
+  }
   k_plan<<<1, 1024, 0, st>>>(a, L.colstat, L.info, L.sum);
   PHB_CUDA_TRY(cudaGetLastError());
   k_rice_chunks<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks);
   PHB_CUDA_TRY(cudaGetLastError());
-  k_rice_chunk_scan<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(ncols, nch, L.chunks);
+  k_rice_chunk_scan<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(ncols, nch, L.chunks,
+                                                               a.rice_totals_out);
   PHB_CUDA_TRY(cudaGetLastError());
   if (host_sum) {
     PHB_CUDA_TRY(cudaMemcpyAsync(host_sum, L.sum, sizeof(EncodeSummary), cudaMemcpyDeviceToHost,
@@ -439,16 +453,32 @@ int launch_encode_write(const EncodeArgs& a, void* ws, uint8_t* blob, size_t blo
   WsLayout L = carve(ws, ncols, nch);
   PHB_CUDA_TRY(cudaMemsetAsync(blob, 0, blob_bytes, st));
   uint32_t* words = reinterpret_cast<uint32_t*>(blob);
-  k_headers<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(a, L.info, L.sum, words);
-  PHB_CUDA_TRY(cudaGetLastError());
+  if (a.write_headers) {
+    k_headers<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(a, L.info, L.sum, words);
+    PHB_CUDA_TRY(cudaGetLastError());
+  }
   int64_t nd = a.nparts_global + 1;
-  if (a.deltas) {
+  if (a.deltas && a.write_headers) {
     k_deltas<<<(unsigned)std::min<int64_t>(cdiv(nd, 256), 4096), 256, 0, st>>>(a.deltas, nd, L.sum,
                                                                         words);
     PHB_CUDA_TRY(cudaGetLastError());
   }
-  Cols cols{a.seeds, a.nparts, a.bcount, a.mono};
-  k_payload<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks, words);
+  Cols cols{a.seeds, a.nparts, a.bcount, a.mono, a.row0 * (a.mono ? (int64_t)a.bcount : 1)};
+  k_payload<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks, a.rice_base,
+                                                    words);
+  return (int)cudaGetLastError();
+}
+
+int launch_encode_stats(const EncodeArgs& a, void* ws, unsigned long long* colstat_out,
+                        cudaStream_t st) {
+  const int64_t ncols = a.mono ? 1 : a.bcount;
+  const int64_t cnt = a.mono ? a.nparts * (int64_t)a.bcount : a.nparts;
+  int64_t nch = cdiv(cnt, ECH);
+  if (nch < 1) nch = 1;
+  (void)ws;
+  PHB_CUDA_TRY(cudaMemsetAsync(colstat_out, 0, (size_t)ncols * 65 * 8, st));
+  Cols cols{a.seeds, a.nparts, a.bcount, a.mono, 0};
+  if (cnt > 0) k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, colstat_out);
   return (int)cudaGetLastError();
 }
 

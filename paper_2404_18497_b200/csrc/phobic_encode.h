@@ -21,6 +21,14 @@ struct EncodeArgs {
   const int64_t* layout_stats;  // device: [0] = max |delta|
   const uint8_t* status;        // optional [nparts]
   const int64_t* part_trials;   // optional [nparts]
+  // sharded (multi-GPU) encoding: this shard holds rows [row0, row0 + nparts)
+  // of a column of count_global values; 0 / null = a whole-matrix encode
+  int64_t row0 = 0;
+  int64_t count_global = 0;            // values per column over all shards
+  const unsigned long long* colstat_in = nullptr;   // reduced stats [ncols][65]
+  unsigned long long* rice_totals_out = nullptr;    // this shard's sum(high + 1) per column
+  const unsigned long long* rice_base = nullptr;    // unary bits of earlier shards per column
+  int write_headers = 1;               // headers + deltas (one shard writes them)
 };
 
 struct ColInfo {
@@ -40,6 +48,8 @@ struct EncodeSummary {
 };
 
 size_t encode_workspace_bytes(int64_t nparts, uint32_t bcount, int mono);
+int launch_encode_stats(const EncodeArgs& a, void* ws, unsigned long long* colstat_out,
+                        cudaStream_t st);
 int launch_encode_plan(const EncodeArgs& a, void* ws, EncodeSummary* host_sum, cudaStream_t st);
 int launch_encode_write(const EncodeArgs& a, void* ws, uint8_t* blob, size_t blob_bytes,
                         cudaStream_t st);

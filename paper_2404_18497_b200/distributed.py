@@ -19,9 +19,11 @@ Per attempt (global_seed + attempt, the reference's retry, mphf.py:251-261):
      one partition-grouped array (a segmented copy, phb_regroup).
   6. K4 search on the owned partitions; all_reduce of the failure flag
      (collective retry) and of the trial count.
-  7. all_gather of the owned seed columns -> every rank assembles the global
-     [B][nparts] seed matrix and runs K5 (replicated; the encoded body is
-     identical on every rank), so every rank holds a queryable Mphf.
+  7. sharded K5: the column statistics are all_reduced, every rank plans the
+     same global geometry and writes its own rows' fields at their global bit
+     addresses, and a uint8 SUM all_reduce ORs the bodies (each bit has one
+     writer), so every rank holds the identical body and a queryable Mphf
+     (encode="gather": all_gather of the seed rows + replicated K5).
 
 The kernels are reached through an ``ops`` object. ``DeviceOps`` (default)
 calls the C-ABI; the CPU tests inject an oracle-backed implementation to
@@ -143,12 +145,53 @@ class DeviceOps:
         return blob, summ
 
 
+    def encode_sharded(self, seeds_own: torch.Tensor, p_lo: int, np_g: int, nparts: int,
+                       deltas, stats, group, rank: int, world: int):
+        """K5 over the ranks' own seed rows (phb_encode_shard_*): reduce the
+        column statistics, plan the global geometry on every rank, write the
+        own fields at their global bit addresses, OR the bodies together (a
+        uint8 SUM, every bit has exactly one writer)."""
+        mono, prefix = self.config.compact_prefix()
+        B = self.B
+        ncols = 1 if mono else B
+        L = _native.lib()
+        P = _native.ptr
+        st = _native.stream()
+        seeds_own = seeds_own.contiguous()
+        colstat = torch.empty(ncols * 65, dtype=torch.int64, device=self.dev)
+        _native.call("phb_encode_shard_stats", P(seeds_own), np_g, B, mono, P(colstat), st)
+        cs = colstat.view(ncols, 65)
+        mx = cs[:, 0].contiguous()   # seeds < 2^63: the int64 view orders like u64
+        pops = cs[:, 1:].contiguous()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+        dist.all_reduce(pops, op=dist.ReduceOp.SUM, group=group)
+        cs_g = torch.cat([mx[:, None], pops], 1).contiguous()
+        ws = torch.empty(int(L.phb_encode_workspace_bytes(max(np_g, 1), B, mono)),
+                         dtype=torch.uint8, device=self.dev)
+        totals = torch.empty(ncols, dtype=torch.int64, device=self.dev)
+        summ = np.zeros(8, np.int64)
+        _native.call("phb_encode_shard_plan", P(seeds_own), np_g, p_lo, nparts, B, mono, prefix,
+                     P(stats), P(cs_g), P(ws), P(totals), summ.ctypes.data_as(ctypes.c_void_p), st)
+        allt = [torch.empty_like(totals) for _ in range(world)]
+        dist.all_gather(allt, totals, group=group)
+        base = torch.zeros_like(totals)
+        for g in range(rank):
+            base += allt[g]
+        total = int(summ[0])
+        blob = torch.empty((total + 16 + 3) // 4 * 4, dtype=torch.uint8, device=self.dev)
+        _native.call("phb_encode_shard_write", P(seeds_own), np_g, p_lo, nparts, B, mono, prefix,
+                     P(deltas), P(stats), P(base), int(rank == 0), P(ws), P(blob), blob.numel(),
+                     st)
+        dist.all_reduce(blob, op=dist.ReduceOp.SUM, group=group)
+        return blob, summ
+
+
 def _as_bytes(t: torch.Tensor) -> torch.Tensor:
     return t.contiguous().view(torch.uint8)
 
 
 def build_distributed(local_keys, config: BuildConfig | None = None, group=None, ops=None,
-                      to_host: bool = True, transport: str = "nccl"):
+                      to_host: bool = True, transport: str = "nccl", encode: str = "sharded"):
     """Collective build: every rank passes its shard; every rank returns the
     same Mphf (global n, identical bytes for any world size). With
     to_host=False the device-resident DeviceBuild is returned instead.
@@ -156,7 +199,12 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
     transport: "nccl" = K3 + all_to_all_single + phb_regroup; "p2p" = the
     fused route, K3 writing every record straight into its owner's buffer
     over CUDA-IPC peer memory (phb_scatter_p2p; one process per GPU on one
-    node)."""
+    node).
+
+    encode: "sharded" (device ops) = every rank encodes its own seed rows at
+    their global bit addresses and the bodies are OR-ed (a uint8 all_reduce
+    of ~bits/key * n / 8 bytes); "gather" = all_gather of the seed rows and a
+    replicated encode (8 B per partition and bucket moved)."""
     from .mphf import BuildStats, DeviceBuild, DuplicateKeys, Mphf
 
     config = config or BuildConfig()
@@ -239,8 +287,19 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
             last = f"partition {gbad}: {reason}"
             continue
         trials_total = int(red[1].item())
-        # 7. all_gather the owned seed columns (padded to the widest range)
         B = config.bucket_count
+        if isinstance(ops, DeviceOps) and encode == "sharded":
+            # 7. sharded encode: no rank assembles the seed matrix
+            blob, summ = ops.encode_sharded(seeds_own, p_lo, np_g, nparts, deltas, stats, group,
+                                            rank, world)
+            stats_obj = BuildStats(attempt + 1, trials_total, trials_total / n,
+                                   time.perf_counter() - t0)
+            db = DeviceBuild(n, nparts, B, seed, key_off_g, deltas, None, blob, int(summ[0]),
+                             int(summ[1]), trials_total)
+            if not to_host:
+                return db
+            return Mphf._from_device(db, config, _EngineView(ops), stats_obj)
+        # 7. all_gather the owned seed columns (padded to the widest range)
         width = max(bounds[g + 1] - bounds[g] for g in range(world))
         pad = torch.zeros((B, width), dtype=torch.int64, device=seeds_own.device)
         pad[:, :np_g] = seeds_own

@@ -252,7 +252,8 @@ class Mphf:
             db = self._dev
             store, _ = parse_section(memoryview(self._body), db.seed_section, db.nparts,
                                      db.bcount)
-            store._device = db.seeds.view(db.bcount, db.nparts)
+            if db.seeds is not None:  # a sharded multi-GPU build keeps no seed matrix
+                store._device = db.seeds.view(db.bcount, db.nparts)
             # encoded blocks for query_encoded_device come from the device body
             store._dev_source = (db.blob, db.seed_section + 4, db.total_bytes)
             self._seeds = store
@@ -282,7 +283,10 @@ class Mphf:
     def _device_state(self, matrix: bool = True):
         dev = _native.require_device()
         if self._dev is not None:
-            return self._dev_key_off, self._dev_entries, self._dev.seeds
+            seeds = self._dev.seeds
+            if seeds is None and matrix:
+                seeds = self.seeds.device_matrix()  # decoded once from the device body
+            return self._dev_key_off, self._dev_entries, seeds
         if self._dev_key_off is None:
             d = torch.from_numpy(np.ascontiguousarray(self.layout.deltas, np.int64)).to(dev)
             key_off = torch.empty(self.layout.num_partitions + 1, dtype=torch.int64, device=dev)

@@ -68,7 +68,7 @@ def test_nccl_world1_equals_single_gpu_build():
     assert f.is_bijection_on(keys)
 
 
-def _dev_worker(rank, world, path, keys, cfg_kw, out_path, transport="nccl"):
+def _dev_worker(rank, world, path, keys, cfg_kw, out_path, transport="nccl", encode="sharded"):
     import torch.distributed as dist
 
     import paper_2404_18497_b200 as phb
@@ -78,7 +78,8 @@ def _dev_worker(rank, world, path, keys, cfg_kw, out_path, transport="nccl"):
     dist.init_process_group("gloo", init_method=f"file://{path}", rank=rank, world_size=world)
     try:
         shards = np.array_split(keys, world)
-        f = build_distributed(shards[rank], phb.BuildConfig(**cfg_kw), transport=transport)
+        f = build_distributed(shards[rank], phb.BuildConfig(**cfg_kw), transport=transport,
+                              encode=encode)
         out = f.query_device(shards[rank])
         ok = bool(((out >= 0) & (out < f.n)).all()) and out.unique().numel() == out.numel()
         outs = [torch.empty(len(s), dtype=torch.int64, device="cuda") for s in shards]
@@ -95,7 +96,7 @@ def _dev_worker(rank, world, path, keys, cfg_kw, out_path, transport="nccl"):
 @pytest.mark.parametrize("world", [2, 3])
 def test_device_sharded_build_gloo_on_one_gpu(world, transport):
     """The DeviceOps path (K1/K3 per shard, all-to-all + phb_regroup or the
-    fused CUDA-IPC peer scatter, K4 on owned partitions, seed all_gather, K5)
+    fused CUDA-IPC peer scatter, K4 on owned partitions, sharded K5)
     with `world` ranks sharing one GPU over gloo: every rank's bytes equal
     the single-GPU build."""
     import torch.multiprocessing as mp
@@ -114,3 +115,27 @@ def test_device_sharded_build_gloo_on_one_gpu(world, transport):
         assert np.load(out + f".{r}.npy").tobytes() == want.serialize()
         ok, trials = np.load(out + f".{r}.ok.npy")
         assert ok and trials == want.stats.trials_total
+
+
+@pytest.mark.parametrize("encoder,encode", [("mono-r", "sharded"), ("ic-c", "sharded"),
+                                            ("mixed:100", "sharded"), ("ic-r", "gather")])
+def test_sharded_encode_every_preset(encoder, encode):
+    """Sharded K5 (column stats all_reduce, per-rank fields at global bit
+    addresses, OR of the bodies) for every preset at world 3: mono-r's one
+    column spans all ranks, so Rice select samples and unary runs cross
+    shard boundaries; "gather" is the all_gather + replicated encode."""
+    import torch.multiprocessing as mp
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.keygen import synth_u64
+
+    keys = synth_u64(300_000, 13)
+    cfg_kw = dict(lambda_=7.0, partition_size=2500.0, encoder=encoder)
+    d = tempfile.mkdtemp()
+    out = os.path.join(d, "blob")
+    world = 3
+    mp.spawn(_dev_worker, args=(world, os.path.join(d, "rdv"), keys, cfg_kw, out, "nccl", encode),
+             nprocs=world)
+    want = phb.build(keys, phb.BuildConfig(**cfg_kw))
+    for r in range(world):
+        assert np.load(out + f".{r}.npy").tobytes() == want.serialize(), (encoder, r)
