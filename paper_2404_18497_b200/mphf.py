@@ -34,7 +34,7 @@ from . import _native
 from .assignment import KIND_CODES, KINDS, AssignmentSpec, AssignmentTable, tabulate
 from .builder import BuildConfig, InvalidConfig, SeedExhausted, device_table
 from .encoders import MonoSeeds, SeedStore, parse_section
-from .keygen import DeviceKeys, as_corpus, to_device
+from .keygen import DeviceKeys, to_device
 from .partitioning import PartitionLayout, num_partitions_for, unpack_deltas
 
 MAGIC = b"PHOB"
