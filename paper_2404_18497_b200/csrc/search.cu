@@ -24,10 +24,17 @@
 //    odd), i.e. 4 shared loads + 3 funnel shifts per key; a ballot + ffs
 //    picks the smallest d. Every 4 keys the warp stops early once all
 //    words are saturated.
+//  * Small buckets test G seeds per step (G = 4 for k <= 8, 2 for k <= 16),
+//    one lane group per seed; the batched instantiations are lean (seeds
+//    >= 1 below the cap, closed-form resolution), the single-seed one keeps
+//    seed 0's duplicate check and the cap. Per-seed hashes of the first 4096
+//    seeds come from a compile-time table.
 //  * Self-collision of a candidate s: __match_any_sync on positions for
 //    k <= 32, shared-memory atomicOr test-and-set for larger buckets.
 //  * Trials use the closed form k * (S_self + sum_fail(dmax+1) + d* + 1),
 //    identical to the reference's per-candidate counting.
+//  * Bound: SM issue / ALU pipe (funnel shift + OR per window word), not HBM
+//    (profiles/search_sm_c2.json); measured alternatives in DESIGN.md §3.
 #include <cstdio>
 #include "common.cuh"
 #include "phobic_internal.h"
