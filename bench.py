@@ -161,7 +161,11 @@ def cpu_baseline(sample_keys: int, threads: int):
     f = oracle.build(keys, lambda_=LAMBDA, P=PSIZE, encoder=ENCODER, threads=threads)
     body = f.body()
     dt = time.perf_counter() - t0
+    import numpy as np
+
+    trials = int(np.asarray(f.trials).sum())
     return {"value": sample_keys / dt, "unit": "keys/s", "cores": threads, "kind": "port",
+            "trials_per_s": trials / dt,
             "sample": f"{sample_keys:,} keys of the same synthetic stream, lambda=9 IC-C, "
                       f"full build (hash, partition, search, encode) in {dt:.2f} s",
             "ns_per_key": dt * 1e9 / sample_keys, "bits_per_key": (len(body) + 57 + 8 - 16) * 8 / sample_keys}
@@ -362,6 +366,11 @@ def run_gpu(args):
                                    f"owners ({args.transport})" if world > 1 else "1 GPU")},
         "ns_per_key": ms * 1e6 / total_keys,
         "bits_per_key": bits,
+        # the reference's work unit (one key x one (s, d) candidate, _kernels.py:236-240)
+        "search_work": {"trials_per_key": res.trials_total / total_keys,
+                        "trials_per_s": res.trials_total / (ms * 1e-3),
+                        "search_trials_per_s": (res.trials_total / (per["phb_search"] * 1e-3)
+                                                if "phb_search" in per else None)},
         "query": {"value": total_keys / (allmax(q_ms, world) * 1e-3) / 1e6, "unit": "Mq/s",
                   "ms": q_ms, "bijection_verified": True,
                   "what": "batched GPU query of every key (hash fused), keys resident",
