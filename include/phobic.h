@@ -195,7 +195,16 @@ int phb_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t
                       int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                       const int64_t* key_off, const double* entries, int32_t bcount,
                       const uint8_t* section, const int64_t* col_info, int32_t num_enc,
-                      int32_t mono, int64_t* out, void* stream);
+                      int32_t mono, const uint32_t* select_dir, int64_t select_stride,
+                      int64_t* out, void* stream);
+
+/* Dense select directory for the Rice encoders of a section (optional input
+ * of phb_query_encoded; NULL there = use the serialized every-1024th
+ * samples): select_dir[e * stride + r] = bit position, within encoder e's
+ * unary highs, of its (64 r)-th one; stride >= ceil(count / 64) of every
+ * Rice encoder. Built once per loaded structure. */
+int phb_select_index(const uint8_t* section, const int64_t* col_info, int64_t num_enc,
+                     int64_t stride, uint32_t* select_dir, void* stream);
 
 /* K8: bijection check onto [0, n): bitmap (ceil(n/32) u32, zeroed by
  * caller) and bad_flag (one u32, zeroed) set to 1 on a repeat or an

@@ -362,12 +362,21 @@ int phb_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t
                       int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                       const int64_t* key_off, const double* entries, int32_t bcount,
                       const uint8_t* section, const int64_t* col_info, int32_t num_enc,
-                      int32_t mono, int64_t* out, void* stream) {
+                      int32_t mono, const uint32_t* select_dir, int64_t select_stride,
+                      int64_t* out, void* stream) {
   if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
   if (nparts < 1 || !section || !col_info) return PHB_E_ARGS;
   if (mono ? num_enc != 1 : num_enc != bcount) return PHB_E_ARGS;
   return launch_query_encoded(buf, offsets, keys64, nq, seed, n, nparts, key_off, entries,
-                              (uint32_t)bcount, section, col_info, mono, out, S(stream));
+                              (uint32_t)bcount, section, col_info, mono, select_dir,
+                              select_stride, out, S(stream));
+}
+
+int phb_select_index(const uint8_t* section, const int64_t* col_info, int64_t num_enc,
+                     int64_t stride, uint32_t* select_dir, void* stream) {
+  if (num_enc < 0 || stride < 1 || (num_enc > 0 && (!section || !col_info || !select_dir)))
+    return PHB_E_ARGS;
+  return launch_select_index(section, col_info, num_enc, stride, select_dir, S(stream));
 }
 
 int phb_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad_flag,

@@ -71,8 +71,10 @@ int launch_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* key
 int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                          int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                          const int64_t* key_off, const double* entries, uint32_t bcount,
-                         const uint8_t* section, const int64_t* cols, int mono, int64_t* out,
-                         cudaStream_t st);
+                         const uint8_t* section, const int64_t* cols, int mono,
+                         const uint32_t* dsel, int64_t dstride, int64_t* out, cudaStream_t st);
+int launch_select_index(const uint8_t* section, const int64_t* cols, int64_t ncols,
+                        int64_t stride, uint32_t* dsel, cudaStream_t st);
 int launch_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad,
                   cudaStream_t st);
 

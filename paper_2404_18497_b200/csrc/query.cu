@@ -103,10 +103,84 @@ __device__ __forceinline__ uint32_t ehigh_word(const uint8_t* blob, const ECol& 
   return (uint32_t)ebits(blob, 8ull * d.highs_byte + 32ull * w, nb < 32 ? (int)nb : 32);
 }
 
-// Select.select1: position of the (k+1)-th one (k >= 0)
-__device__ int64_t eselect1(const uint8_t* blob, const ECol& d, int64_t k) {
-  const int64_t spos = (int64_t)ebits(blob, 8ull * d.samples_byte + 64ull * (k >> 10), 64);
-  int need = (int)(k & 1023) + 1;
+// Dense select directory (built on the device once per loaded structure):
+// dsel[c * stride + r] = position of the (64 r)-th one of Rice column c, so
+// a select scans at most 63 ones instead of up to 1023 from the serialized
+// every-1024th samples. One CTA per column.
+constexpr int DS_STEP = 64;
+__global__ void __launch_bounds__(256) k_select_index(const uint8_t* __restrict__ sec,
+                                                      const ECol* __restrict__ cols,
+                                                      int64_t stride, uint32_t* __restrict__ dsel) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint64_t carry;
+  const ECol d = cols[blockIdx.x];
+  if (d.kind != 1 || d.param >= 64) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int64_t nw = (d.highs_nbits + 31) / 32;
+  constexpr int WPT = 8;
+  uint32_t* row = dsel + (int64_t)blockIdx.x * stride;
+  for (int64_t w0 = 0; w0 < nw; w0 += 256 * WPT) {
+    const int64_t wb = w0 + (int64_t)threadIdx.x * WPT;
+    uint32_t words[WPT], local = 0;
+#pragma unroll
+    for (int e = 0; e < WPT; ++e) {
+      words[e] = wb + e < nw ? ehigh_word(sec, d, wb + e) : 0u;
+      local += __popc(words[e]);
+    }
+    uint32_t inc = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t x = lane < 8 ? wsum[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      if (lane < 8) wsum[lane] = x;
+    }
+    __syncthreads();
+    uint64_t rank = carry + (wid ? wsum[wid - 1] : 0u) + inc - local;
+#pragma unroll
+    for (int e = 0; e < WPT; ++e) {
+      uint32_t x = words[e];
+      const uint32_t c = __popc(x);
+      // ones with rank r = 0 (mod 64) inside this word
+      uint64_t r = (rank + DS_STEP - 1) / DS_STEP * DS_STEP;
+      while (r < rank + c) {
+        uint32_t y = x;
+        for (uint64_t q = rank; q < r; ++q) y &= y - 1;
+        row[r / DS_STEP] = (uint32_t)(32 * (wb + e) + (__ffs(y) - 1));
+        r += DS_STEP;
+      }
+      rank += c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 255) carry = rank;
+    __syncthreads();
+  }
+}
+
+// Select.select1: position of the (k+1)-th one (k >= 0); from the dense
+// directory when there is one, else from the serialized samples
+__device__ int64_t eselect1(const uint8_t* blob, const ECol& d, int64_t k,
+                            const uint32_t* __restrict__ drow) {
+  int64_t spos;
+  int need;
+  if (drow) {
+    spos = __ldg(drow + (k >> 6));
+    need = (int)(k & 63) + 1;
+  } else {
+    spos = (int64_t)ebits(blob, 8ull * d.samples_byte + 64ull * (k >> 10), 64);
+    need = (int)(k & 1023) + 1;
+  }
   int64_t w = spos >> 5;
   uint32_t word = ehigh_word(blob, d, w) & (0xffffffffu << (spos & 31));
   for (;;) {
@@ -128,7 +202,8 @@ __device__ int64_t enext_one(const uint8_t* blob, const ECol& d, int64_t pos) {
   return 32 * w + (__ffs(word) - 1);
 }
 
-__device__ __forceinline__ uint64_t eget(const uint8_t* blob, const ECol* dp, int64_t i) {
+__device__ __forceinline__ uint64_t eget(const uint8_t* blob, const ECol* dp, int64_t i,
+                                         const uint32_t* drow) {
   // only {kind, param} and {count, payload} are read for Compact columns
   const longlong2 kp = __ldg(reinterpret_cast<const longlong2*>(dp));
   const int64_t pay = __ldg(&dp->pay_byte);
@@ -140,7 +215,7 @@ __device__ __forceinline__ uint64_t eget(const uint8_t* blob, const ECol* dp, in
   const uint64_t low = b ? ebits(blob, 8ull * pay + (uint64_t)i * b, b) : 0ull;
   if (b >= 64) return low;
   const ECol d = *dp;
-  const int64_t prev = i > 0 ? eselect1(blob, d, i - 1) : -1;
+  const int64_t prev = i > 0 ? eselect1(blob, d, i - 1, drow) : -1;
   const int64_t pos = enext_one(blob, d, prev + 1);
   return ((uint64_t)(pos - prev - 1) << b) | low;
 }
@@ -152,7 +227,7 @@ __global__ void __launch_bounds__(256)
                 uint64_t nparts, const int64_t* __restrict__ key_off,
                 const double* __restrict__ entries, uint32_t bcount,
                 const uint8_t* __restrict__ sec, const ECol* __restrict__ cols, int mono,
-                int64_t* __restrict__ out) {
+                const uint32_t* __restrict__ dsel, int64_t dstride, int64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
        i += (int64_t)gridDim.x * blockDim.x) {
     Hash128 h;
@@ -170,8 +245,9 @@ __global__ void __launch_bounds__(256)
       r = offj < n ? offj : n - 1;
     } else {
       const uint32_t b = bucket_of(entries, h.hi, bcount);
-      const uint64_t p = mono ? eget(sec, cols, (int64_t)j * bcount + (b - 1))
-                              : eget(sec, cols + (b - 1), (int64_t)j);
+      const uint64_t p =
+          mono ? eget(sec, cols, (int64_t)j * bcount + (b - 1), dsel)
+               : eget(sec, cols + (b - 1), (int64_t)j, dsel ? dsel + (int64_t)(b - 1) * dstride : nullptr);
       const uint64_t mu = (uint64_t)m;
       const uint64_t s = p / mu;
       const uint64_t d = p - s * mu;
@@ -229,17 +305,25 @@ int launch_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* key
 int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                          int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                          const int64_t* key_off, const double* entries, uint32_t bcount,
-                         const uint8_t* section, const int64_t* cols, int mono, int64_t* out,
-                         cudaStream_t st) {
+                         const uint8_t* section, const int64_t* cols, int mono,
+                         const uint32_t* dsel, int64_t dstride, int64_t* out, cudaStream_t st) {
   if (nq <= 0) return 0;
   const int g = qgrid(nq);
   const ECol* c = reinterpret_cast<const ECol*>(cols);
   if (keys64)
     k_query_enc<0><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
-                                      entries, bcount, section, c, mono, out);
+                                      entries, bcount, section, c, mono, dsel, dstride, out);
   else
     k_query_enc<1><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
-                                      entries, bcount, section, c, mono, out);
+                                      entries, bcount, section, c, mono, dsel, dstride, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_select_index(const uint8_t* section, const int64_t* cols, int64_t ncols,
+                        int64_t stride, uint32_t* dsel, cudaStream_t st) {
+  if (ncols <= 0) return 0;
+  k_select_index<<<(unsigned)ncols, 256, 0, st>>>(section, reinterpret_cast<const ECol*>(cols),
+                                                  stride, dsel);
   return (int)cudaGetLastError();
 }
 

@@ -214,6 +214,19 @@ def _device_blocks(store):
     return store._dev_blocks
 
 
+def _select_dir(d_blob, d_info, hinfo: np.ndarray):
+    """(dense select directory, stride) for the Rice encoders (phb_select_index),
+    or (None, 1) when the section has none."""
+    rice = hinfo[:, 0] == 1
+    if not rice.any():
+        return None, 1
+    stride = int((hinfo[rice, 2].max() + 63) // 64) + 1
+    dsel = torch.zeros(len(hinfo) * stride, dtype=torch.int32, device=d_blob.device)
+    _native.call("phb_select_index", _native.ptr(d_blob), _native.ptr(d_info), len(hinfo), stride,
+                 _native.ptr(dsel), _native.stream())
+    return dsel, stride
+
+
 def _decode(store, nparts: int, bcount: int, mono: bool) -> torch.Tensor:
     """Device decode -> column-major u64 matrix [bcount][nparts] (torch int64 view)."""
     dev = _native.require_device()
@@ -260,8 +273,8 @@ class InterleavedSeeds:
     def device_encoded(self):
         """(section blob, col_info, num encoders, mono) on the device, cached."""
         if self._encoded is None:
-            blob, info, _ = _device_blocks(self)
-            self._encoded = (blob, info, len(self.encoders), 0)
+            blob, info, hinfo = _device_blocks(self)
+            self._encoded = (blob, info, len(self.encoders), 0) + _select_dir(blob, info, hinfo)
         return self._encoded
 
     def decode_matrix(self) -> np.ndarray:
@@ -311,8 +324,8 @@ class MonoSeeds:
 
     def device_encoded(self):
         if self._encoded is None:
-            blob, info, _ = _device_blocks(self)
-            self._encoded = (blob, info, 1, 1)
+            blob, info, hinfo = _device_blocks(self)
+            self._encoded = (blob, info, 1, 1) + _select_dir(blob, info, hinfo)
         return self._encoded
 
     def decode_matrix(self) -> np.ndarray:

@@ -322,7 +322,7 @@ class Mphf:
         encoders.py:89-99, :224-230) instead of a decoded seed matrix."""
         dev = _native.require_device()
         key_off, entries, _ = self._device_state(matrix=False)
-        blob, info, num_enc, mono = self.seeds.device_encoded()
+        blob, info, num_enc, mono, dsel, dstride = self.seeds.device_encoded()
         dk = keys if isinstance(keys, DeviceKeys) else to_device(keys, dev)
         out = torch.empty(dk.n, dtype=torch.int64, device=dev)
         P = _native.ptr
@@ -330,7 +330,7 @@ class Mphf:
                      None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
                      dk.n, self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n, self.num_partitions,
                      P(key_off), P(entries), self.bcount, P(blob), P(info), num_enc, mono,
-                     P(out), _native.stream())
+                     None if dsel is None else P(dsel), dstride, P(out), _native.stream())
         return out
 
     def query_many(self, keys) -> np.ndarray:

@@ -82,3 +82,26 @@ def test_encoded_query_c2_scale(phb):
     assert f.verify_device(out)
     sample = keys[::997].contiguous()
     assert torch.equal(out[::997], f.query_device(DeviceKeys(sample.numel(), keys64=sample)))
+
+
+def test_encoded_query_without_select_directory(phb):
+    """phb_query_encoded with select_dir = NULL scans from the serialized
+    every-1024th samples; same outputs as with the dense directory."""
+    from paper_2404_18497_b200 import _native
+
+    rng = np.random.default_rng(17)
+    keys = np.unique(rng.integers(0, 2**64, size=200_000, dtype=np.uint64))
+    f = phb.build(keys, phb.BuildConfig(lambda_=5.0, partition_size=300.0, encoder="mono-r"))
+    dk = torch.from_numpy(keys.view(np.int64)).cuda()
+    with_dir = f.query_encoded_device(dk)
+    key_off, entries, _ = f._device_state(matrix=False)
+    blob, info, num_enc, mono, dsel, _ = f.seeds.device_encoded()
+    assert dsel is not None
+    out = torch.empty_like(with_dir)
+    P = _native.ptr
+    _native.call("phb_query_encoded", None, None, P(dk), dk.numel(),
+                 f.global_seed & 0xFFFFFFFFFFFFFFFF, f.n, f.num_partitions, P(key_off),
+                 P(entries), f.bcount, P(blob), P(info), num_enc, mono, None, 1, P(out),
+                 _native.stream())
+    assert torch.equal(out, with_dir)
+    assert torch.equal(with_dir, f.query_device(dk))
