@@ -139,3 +139,23 @@ def test_sharded_encode_every_preset(encoder, encode):
     want = phb.build(keys, phb.BuildConfig(**cfg_kw))
     for r in range(world):
         assert np.load(out + f".{r}.npy").tobytes() == want.serialize(), (encoder, r)
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_sharded_build_rank_without_partitions(transport):
+    """2 partitions over 3 ranks: the last rank owns no partition (empty
+    search, empty encode shard) and still returns the identical structure."""
+    import torch.multiprocessing as mp
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.keygen import synth_u64
+
+    keys = synth_u64(999, 21)  # equal shards (the harness all_gathers query outputs)
+    cfg_kw = dict(lambda_=4.0, partition_size=500.0, encoder="ic-r")
+    d = tempfile.mkdtemp()
+    out = os.path.join(d, "blob")
+    mp.spawn(_dev_worker, args=(3, os.path.join(d, "rdv"), keys, cfg_kw, out, transport),
+             nprocs=3)
+    want = phb.build(keys, phb.BuildConfig(**cfg_kw))
+    for r in range(3):
+        assert np.load(out + f".{r}.npy").tobytes() == want.serialize(), r
