@@ -35,7 +35,21 @@ __host__ __device__ constexpr uint64_t mix64(uint64_t z) {
 __device__ __forceinline__ uint64_t mulhi(uint64_t z, uint64_t m) { return __umul64hi(z, m); }
 
 __host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
+#ifdef __CUDA_ARCH__
+  // two 32-bit funnel shifts (the generic 64-bit form compiles to ~4 ops)
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  uint32_t nhi, nlo;
+  if (r < 32) {
+    nhi = __funnelshift_l(lo, hi, r);
+    nlo = __funnelshift_l(hi, lo, r);
+  } else {
+    nhi = __funnelshift_l(hi, lo, r - 32);
+    nlo = __funnelshift_l(lo, hi, r - 32);
+  }
+  return ((uint64_t)nhi << 32) | nlo;
+#else
   return (x << r) | (x >> (64 - r));
+#endif
 }
 
 __host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
