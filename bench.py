@@ -395,6 +395,10 @@ def run_gpu(args):
                          "warp_instructions_per_key": round(sm["warp_instructions"] / 1e8, 1),
                          "source": "profiles/search_sm_c2.json"}},
         "passes": passes,
+        # whole-build floor = 28 B/key of algorithmic traffic at peak HBM
+        "build_roofline": {"algorithmic_bytes_per_key": ALGO_BYTES["total"],
+                           "t_floor_ms": n * ALGO_BYTES["total"] / (hbm * 1e9) * 1e3,
+                           "frac": (n * ALGO_BYTES["total"] / (hbm * 1e9) * 1e3) / ms},
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
