@@ -261,3 +261,22 @@ def test_staged_ingestion_equals_device_keys(phb):
     assert a == b
     padded = staged_h2d(np.arange(5, dtype=np.uint8), dev_keys.device, pad=11)
     assert padded.numel() == 16 and padded[5:].sum().item() == 0
+
+
+def test_bench_workload_slice_vs_oracle(phb, orc):
+    """The bench workload's own keys (mix64(i), C2 parameters lambda = 9,
+    P = 2500, IC-C) on an 8M-key slice: bytes, trial total and queries equal
+    the oracle's; the oracle runs on all host cores."""
+    import os
+
+    from paper_2404_18497_b200.keygen import synth_u64
+
+    keys = synth_u64(8_000_000, 0)
+    cfg = phb.BuildConfig(lambda_=9.0, partition_size=2500.0, encoder="ic-c")
+    f = phb.build(keys, cfg)
+    ref = orc.build(keys, lambda_=9.0, P=2500.0, encoder="ic-c", threads=os.cpu_count() or 1)
+    assert f.serialize() == ref.serialize()
+    assert f.stats.trials_total == int(ref.trials.sum())
+    hi, lo = orc.murmur3_u64(keys[:200_000], f.global_seed)
+    assert np.array_equal(f.query_many(keys[:200_000]), ref.query_hashes(hi, lo))
+    assert f.is_bijection_on(keys)
