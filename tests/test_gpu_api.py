@@ -280,3 +280,47 @@ def test_bench_workload_slice_vs_oracle(phb, orc):
     hi, lo = orc.murmur3_u64(keys[:200_000], f.global_seed)
     assert np.array_equal(f.query_many(keys[:200_000]), ref.query_hashes(hi, lo))
     assert f.is_bijection_on(keys)
+
+
+@pytest.mark.parametrize("case", range(30))
+def test_random_configs_vs_oracle(phb, orc, case):
+    """Randomised configurations (lambda, partition size, encoder preset, tie
+    order, global seed, key count) against the oracle: bytes, trials and the
+    bijection."""
+    rng = np.random.default_rng(1000 + case)
+    lam = float(rng.choice([2.5, 3.9, 4.5, 5.0, 6.5, 7.0, 8.0, 9.0, 10.0]))
+    P = float(rng.choice([100.0, 500.0, 1000.0, 2500.0, 3000.0]))
+    enc = str(rng.choice(["ic-c", "ic-r", "mono-c", "mono-r", "mixed:7", "mixed:50"]))
+    tie = str(rng.choice(["asc-expected", "desc-expected"]))
+    gseed = int(rng.integers(0, 2**63))
+    n = int(rng.integers(20_000, 200_000))
+    keys = np.unique(rng.integers(0, 2**64, size=n, dtype=np.uint64))
+    cfg = phb.BuildConfig(lambda_=lam, partition_size=P, encoder=enc, tie_break=tie,
+                          global_seed=gseed)
+    f = phb.build(keys, cfg)
+    ref = orc.build(keys, lambda_=lam, P=P, encoder=enc, tie_break=tie, global_seed=gseed)
+    assert f.serialize() == ref.serialize(), (lam, P, enc, tie, gseed, n)
+    assert f.stats.trials_total == int(ref.trials.sum())
+    assert f.is_bijection_on(keys)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_random_string_configs_vs_oracle(phb, orc, case):
+    """Randomised configurations over variable-length byte keys (0-120 B,
+    full byte range, duplicates removed) against the oracle."""
+    rng = np.random.default_rng(2000 + case)
+    n = int(rng.integers(5_000, 60_000))
+    lens = rng.integers(0, 121, size=n)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    buf = rng.integers(0, 256, size=int(off[-1]), dtype=np.uint8)
+    uniq = {bytes(buf[off[i]:off[i + 1]]) for i in range(n)}
+    keys = sorted(uniq)
+    corpus = phb.KeyCorpus.from_keys(keys)
+    lam = float(rng.choice([3.0, 5.0, 8.0]))
+    P = float(rng.choice([200.0, 1000.0, 2500.0]))
+    enc = str(rng.choice(["ic-c", "ic-r", "mono-r", "mixed:9"]))
+    f = phb.build(corpus, phb.BuildConfig(lambda_=lam, partition_size=P, encoder=enc))
+    ref = orc.build((corpus.buf, corpus.offsets), lambda_=lam, P=P, encoder=enc)
+    assert f.serialize() == ref.serialize(), (lam, P, enc, n)
+    assert f.is_bijection_on(corpus)
