@@ -42,8 +42,10 @@ LAMBDA = 9.0
 PSIZE = 2500.0
 ENCODER = "ic-c"
 PUBLISHED_NS_PER_KEY = 28.0  # PHOBIC-GPU lambda=9 IC-C, RTX 3090
-ALGO_BYTES = {"total": 28, "hash_count": 8, "scatter": 18, "search": 10}  # SURVEY.md §8(d), per key
-KERNELS_PER_BUILD = 12  # hash_count, layout, cursor_init, scatter, search, 7 encode kernels
+# SURVEY.md §8(d), per key: the grouping pass reads the key (8 B) and writes
+# (lo, bucket id) (10 B); the search reads the record (10 B)
+ALGO_BYTES = {"total": 28, "hash_count": 8, "scatter": 18, "group": 18, "search": 10}
+KERNELS_PER_BUILD = 12  # padded_init, scatter_padded, padded_counts, layout, search, 7 encode
 # (profiles/r1_launches_c2.csv: the ncu launch list of one build, plus two torch zero-fills)
 
 
@@ -215,7 +217,8 @@ def run_gpu(args):
     L = _native.lib()
     stage = {}
     wrapped = {}
-    for name in ("phb_hash_count", "phb_scatter", "phb_search"):
+    for name in ("phb_hash_count", "phb_scatter", "phb_search", "phb_scatter_padded",
+                 "phb_search_strided"):
         fn = getattr(L, name)
 
         def mk(fn, name):
@@ -327,10 +330,15 @@ def run_gpu(args):
 
     peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
+    # the single-GPU build groups into fixed-capacity slots and searches them
+    # strided; the multi-GPU path uses the counted kernels
+    if "phb_search_strided" in per:
+        per["phb_search"] = per.pop("phb_search_strided")
     s_ms = per.get("phb_search", float("nan"))
     achieved = n * ALGO_BYTES["search"] / (s_ms * 1e-3) / 1e9
     passes = {}
-    for k, nm in (("phb_hash_count", "hash_count"), ("phb_scatter", "scatter")):
+    for k, nm in (("phb_hash_count", "hash_count"), ("phb_scatter", "scatter"),
+                  ("phb_scatter_padded", "group")):
         if k in per:
             gbs = n * ALGO_BYTES[nm] / (per[k] * 1e-3) / 1e9
             passes[nm] = {"ms": round(per[k], 4), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)}

@@ -119,6 +119,31 @@ int phb_search(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off, 
                int64_t* part_trials, uint8_t* status, uint64_t* glo, uint32_t* queue,
                void* stream);
 
+/* K3 into fixed-capacity partition slots, for u64 keys arriving in chunks
+ * (no counting pass first): partition j's records go to [j*cap, j*cap + cap)
+ * of lo_out / bid_out through cursor[j] (init != 0 on the first chunk sets
+ * cursor[j] = j*cap; nparts*cap < 2^32). phb_padded_counts then turns the
+ * cursors into the exact per-partition counts (input of phb_layout) and sets
+ * *overflow if any partition exceeded cap (records past it are dropped: the
+ * caller falls back to phb_hash_count + phb_layout + phb_scatter). keys64
+ * must be 16-byte aligned. */
+int phb_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, int64_t nparts,
+                       const double* entries, int32_t bcount, int32_t cap, int32_t init,
+                       uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
+                       uint32_t* overflow, void* stream);
+int phb_padded_counts(const uint32_t* cursor, int64_t nparts, int32_t cap, uint32_t* counts,
+                      uint32_t* overflow, void* stream);
+
+/* K4 over records laid out with a fixed stride (phb_scatter_padded): the
+ * records of partition j start at (j - p_lo) * rec_stride; key_off still
+ * gives the exact offsets (sizes m = key_off[j+1] - key_off[j]). */
+int phb_search_strided(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off,
+                       int64_t p_lo, int64_t p_hi, int64_t out_base, int32_t bcount,
+                       int64_t seed_cap, int32_t tie_desc, int64_t m_max, uint64_t* seeds,
+                       int64_t s_sj, int64_t s_sb, int64_t* trials, int64_t* part_trials,
+                       uint8_t* status, uint64_t* glo, uint32_t* queue, int64_t rec_stride,
+                       void* stream);
+
 /* K5/K6: interleaved / mono Compact-Rice encoding of a column-major seed
  * matrix seeds[bcount][nparts] plus the packed deltas, into the serialized
  * body of Mphf.serialize (mphf.py:156-175) from byte 57 on (the fixed header

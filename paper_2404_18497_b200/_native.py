@@ -33,6 +33,10 @@ SIGNATURES = {
     "phb_hash_count": [P, P, P, I64, U64, I64, P, P],
     "phb_layout": [P, I64, I64, I64, I64, I64, P, P, P, P],
     "phb_scatter": [P, P, P, I64, U64, I64, P, I32, P, P, P, P, P],
+    "phb_scatter_padded": [P, I64, U64, I64, P, I32, I32, I32, P, P, P, P, P],
+    "phb_padded_counts": [P, I64, I32, P, P, P],
+    "phb_search_strided": [P, P, P, I64, I64, I64, I32, I64, I32, I64, P, I64, I64, P, P, P, P, P,
+                           I64, P],
     "phb_search": [P, P, P, I64, I64, I64, I32, I64, I32, I64, P, I64, I64, P, P, P, P, P, P],
     "phb_encode_plan": [P, I64, I32, I32, I32, P, I64, P, P, P, P, P, P],
     "phb_encode_write": [P, I64, I32, I32, I32, P, I64, P, P, P, SZ, P],

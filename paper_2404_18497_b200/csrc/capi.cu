@@ -154,6 +154,54 @@ int phb_search(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off, 
   return launch_search(a, S(stream));
 }
 
+int phb_search_strided(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off,
+                       int64_t p_lo, int64_t p_hi, int64_t out_base, int32_t bcount,
+                       int64_t seed_cap, int32_t tie_desc, int64_t m_max, uint64_t* seeds,
+                       int64_t s_sj, int64_t s_sb, int64_t* trials, int64_t* part_trials,
+                       uint8_t* status, uint64_t* glo, uint32_t* queue, int64_t rec_stride,
+                       void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (rec_stride < 0 || (rec_stride > 0 && m_max > rec_stride)) return PHB_E_ARGS;
+  SearchArgs a;
+  a.lo = lo;
+  a.bid = bid;
+  a.key_off = key_off;
+  a.p_lo = p_lo;
+  a.p_hi = p_hi;
+  a.out_base = out_base;
+  a.bcount = (uint32_t)bcount;
+  a.seed_cap = seed_cap;
+  a.tie_desc = tie_desc;
+  a.seeds = seeds;
+  a.s_sj = s_sj;
+  a.s_sb = s_sb;
+  a.trials = trials;
+  a.part_trials = part_trials;
+  a.status = status;
+  a.glo = glo;
+  a.queue = queue;
+  a.m_max = m_max;
+  a.rec_stride = rec_stride;
+  return launch_search(a, S(stream));
+}
+
+int phb_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, int64_t nparts,
+                       const double* entries, int32_t bcount, int32_t cap, int32_t init,
+                       uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
+                       uint32_t* overflow, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (n < 0 || nparts < 1 || cap < 1 || !cursor || !overflow || (n > 0 && !keys64))
+    return PHB_E_ARGS;
+  return launch_scatter_padded(keys64, n, seed, (uint64_t)nparts, entries, (uint32_t)bcount,
+                               (uint32_t)cap, init, cursor, lo_out, bid_out, overflow, S(stream));
+}
+
+int phb_padded_counts(const uint32_t* cursor, int64_t nparts, int32_t cap, uint32_t* counts,
+                      uint32_t* overflow, void* stream) {
+  if (nparts < 1 || cap < 1 || !cursor || !counts || !overflow) return PHB_E_ARGS;
+  return launch_padded_counts(cursor, nparts, (uint32_t)cap, counts, overflow, S(stream));
+}
+
 int phb_build_partition_range(const uint64_t* his, const uint64_t* los, const int64_t* key_off,
                               int64_t p_lo, int64_t p_hi, const double* entries, int32_t bcount,
                               int64_t seed_cap, int32_t tie_desc, uint64_t* seeds_out,

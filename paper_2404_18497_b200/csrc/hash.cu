@@ -137,6 +137,75 @@ __global__ void __launch_bounds__(256) k_scatter_u64x4(const ulonglong2* __restr
   }
 }
 
+// ---- K3 into fixed-capacity partition slots (no K1 pass before it).
+// Partition j owns records [j * cap, j * cap + cap); its cursor starts at
+// j * cap. The keys can arrive in chunks (one launch per chunk, overlapped
+// with the host-to-device copy of the next); the exact per-partition counts
+// are the cursors afterwards (phb_padded_counts), which also flags a
+// partition that overflowed its capacity (the caller then falls back to
+// the counted layout: K1 + K2 + K3).
+__global__ void k_padded_init(int64_t nparts, uint32_t cap, uint32_t* __restrict__ cursor) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nparts;
+       j += (int64_t)gridDim.x * blockDim.x)
+    cursor[j] = (uint32_t)(j * cap);
+}
+
+__global__ void __launch_bounds__(256) k_scatter_padded_u64x4(
+    const ulonglong2* __restrict__ keys2, int64_t n, uint64_t seed, uint64_t nparts,
+    const double* __restrict__ entries, uint32_t bcount, uint32_t cap,
+    uint32_t* __restrict__ cursor, uint64_t* __restrict__ lo_out, uint16_t* __restrict__ bid_out,
+    uint32_t* __restrict__ overflow) {
+  const int64_t nq = n >> 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 a = __ldg(keys2 + 2 * q), c = __ldg(keys2 + 2 * q + 1);
+    const uint64_t k[4] = {a.x, a.y, c.x, c.y};
+    uint32_t pos[4], b[4], lim[4];
+    uint64_t lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const Hash128 h = murmur3_u64(k[e], seed);
+      const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
+      lo[e] = h.lo;
+      b[e] = bucket_of(entries, h.hi, bcount);
+      lim[e] = (j + 1) * cap;
+      pos[e] = atomicAdd(cursor + j, 1u);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (pos[e] < lim[e]) {
+        lo_out[pos[e]] = lo[e];
+        bid_out[pos[e]] = (uint16_t)b[e];
+      } else {
+        atomicOr(overflow, 1u);
+      }
+    }
+  }
+  const int64_t t = (nq << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) {
+    const uint64_t* keys = reinterpret_cast<const uint64_t*>(keys2);
+    const Hash128 h = murmur3_u64(__ldg(keys + t), seed);
+    const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
+    const uint32_t pos = atomicAdd(cursor + j, 1u);
+    if (pos < (j + 1) * cap) {
+      lo_out[pos] = h.lo;
+      bid_out[pos] = (uint16_t)bucket_of(entries, h.hi, bcount);
+    } else {
+      atomicOr(overflow, 1u);
+    }
+  }
+}
+
+__global__ void k_padded_counts(const uint32_t* __restrict__ cursor, int64_t nparts, uint32_t cap,
+                                uint32_t* __restrict__ counts, uint32_t* __restrict__ overflow) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nparts;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = cursor[j] - (uint32_t)(j * cap);
+    counts[j] = c;
+    if (c > cap) atomicOr(overflow, 1u);
+  }
+}
+
 __global__ void k_cursor_init(const int64_t* __restrict__ key_off, int64_t nparts,
                               uint32_t* __restrict__ cursor) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nparts;
@@ -263,6 +332,31 @@ int launch_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
     k_scatter<<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, entries, bcount,
                                  cursor, lo_out, bid_out);
   }
+  return (int)cudaGetLastError();
+}
+
+int launch_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, uint64_t nparts,
+                          const double* entries, uint32_t bcount, uint32_t cap, int init,
+                          uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
+                          uint32_t* overflow, cudaStream_t st) {
+  if ((uint64_t)nparts * cap >= (uint64_t(1) << 32)) return 1003;  // u32 cursors
+  if (init) {
+    k_padded_init<<<(int)std::min<uint64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+        (int64_t)nparts, cap, cursor);
+    PHB_CUDA_TRY(cudaGetLastError());
+  }
+  if (n <= 0) return 0;
+  if (!aligned16(keys64)) return 1003;
+  k_scatter_padded_u64x4<<<grid_for((n + 3) / 4), 256, 0, st>>>(
+      reinterpret_cast<const ulonglong2*>(keys64), n, seed, nparts, entries, bcount, cap, cursor,
+      lo_out, bid_out, overflow);
+  return (int)cudaGetLastError();
+}
+
+int launch_padded_counts(const uint32_t* cursor, int64_t nparts, uint32_t cap, uint32_t* counts,
+                         uint32_t* overflow, cudaStream_t st) {
+  k_padded_counts<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+      cursor, nparts, cap, counts, overflow);
   return (int)cudaGetLastError();
 }
 

@@ -13,6 +13,12 @@ int launch_murmur(const uint8_t* buf, const int64_t* offsets, const uint64_t* ke
 int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                       int64_t n, uint64_t seed, uint64_t nparts, uint32_t* counts,
                       cudaStream_t st);
+int launch_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, uint64_t nparts,
+                          const double* entries, uint32_t bcount, uint32_t cap, int init,
+                          uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
+                          uint32_t* overflow, cudaStream_t st);
+int launch_padded_counts(const uint32_t* cursor, int64_t nparts, uint32_t cap, uint32_t* counts,
+                         uint32_t* overflow, cudaStream_t st);
 int launch_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
                    uint64_t seed, uint64_t nparts, const double* entries, uint32_t bcount,
                    const int64_t* key_off, uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
@@ -58,6 +64,7 @@ struct SearchArgs {
   uint64_t* glo;           // scratch, indexed like lo
   uint32_t* queue;         // zeroed work counter
   int64_t m_max;           // largest partition size in the range
+  int64_t rec_stride = 0;  // >0: partition j's records start at (j - p_lo) * rec_stride
 };
 int launch_search(const SearchArgs& a, cudaStream_t st);
 

@@ -567,8 +567,9 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     }
     const int64_t j = a.p_lo + t;
     const int64_t row = j - a.out_base;
-    const int64_t kb = a.key_off[j];
-    const uint32_t m = (uint32_t)(a.key_off[j + 1] - kb);
+    const int64_t o0 = a.key_off[j];
+    const uint32_t m = (uint32_t)(a.key_off[j + 1] - o0);
+    const int64_t kb = a.rec_stride ? (j - a.p_lo) * a.rec_stride : o0;  // records of j
     if (m == 0) {  // empty partitions are skipped (_kernels.py:248-249)
       if (lane == 0) {
         a.status[row] = 0;

@@ -155,6 +155,38 @@ def _staged_copy(src: np.ndarray, out: torch.Tensor, nbytes: int, device) -> Non
         st["events"][slot] = ev
 
 
+_COPY_CHUNK_KEYS = 8 << 20  # 64 MB of u64 keys per chunk (even: 16-byte aligned chunk starts)
+_copy_streams: dict = {}
+
+
+def to_device_chunked(keys, device: torch.device):
+    """(DeviceKeys, chunks) for pinned host u64 tensors: the copy is issued as
+    chunks on a side stream, chunks = [(begin, end, event)], so the grouping
+    pass can consume each chunk as soon as it lands (BuildEngine.run). Any
+    other input: (to_device(keys), None)."""
+    if (isinstance(keys, torch.Tensor) and not keys.is_cuda and keys.is_pinned()
+            and keys.dtype in (torch.int64, torch.uint64) and keys.dim() == 1
+            and keys.is_contiguous() and keys.numel() > _COPY_CHUNK_KEYS):
+        n = keys.numel()
+        out = torch.empty(n, dtype=torch.int64, device=device)
+        src = keys.view(torch.int64)
+        cs = _copy_streams.get(device)
+        if cs is None:
+            cs = _copy_streams[device] = torch.cuda.Stream(device)
+        cs.wait_stream(torch.cuda.current_stream(device))  # `out` is allocated on the compute stream
+        chunks = []
+        with torch.cuda.stream(cs):
+            for a in range(0, n, _COPY_CHUNK_KEYS):
+                b = min(a + _COPY_CHUNK_KEYS, n)
+                out[a:b].copy_(src[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                chunks.append((a, b, ev))
+        out.record_stream(cs)
+        return DeviceKeys(n, keys64=out, h2d_bytes=n * 8), chunks
+    return to_device(keys, device), None
+
+
 def _host_to_device_u64(t: torch.Tensor, device: torch.device) -> torch.Tensor:
     if t.is_cuda:
         return t.to(device)

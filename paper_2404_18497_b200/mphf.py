@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import math
 import struct
 import time
 from dataclasses import dataclass
@@ -34,7 +35,7 @@ from . import _native
 from .assignment import KIND_CODES, KINDS, AssignmentSpec, AssignmentTable, tabulate
 from .builder import BuildConfig, InvalidConfig, SeedExhausted, device_table
 from .encoders import MonoSeeds, SeedStore, parse_section
-from .keygen import DeviceKeys, to_device
+from .keygen import DeviceKeys, to_device, to_device_chunked
 from .partitioning import PartitionLayout, num_partitions_for, unpack_deltas
 
 MAGIC = b"PHOB"
@@ -119,14 +120,61 @@ class BuildEngine:
         self.bcount = config.bucket_count
         self.mono, self.prefix = config.compact_prefix()
         self._pinned = torch.zeros(2, dtype=torch.int64).pin_memory()
+        self._pinned3 = torch.zeros(3, dtype=torch.int64).pin_memory()
         self._summary = np.zeros(8, np.int64)
         self.last_launches = 0
 
-    def run(self, dk: DeviceKeys, seed: int,
-            instrument: bool = False) -> DeviceBuild | tuple[int, int]:
+    def padded_capacity(self, n: int) -> int:
+        """Record slots per partition for the fixed-capacity grouping: the
+        mean size plus 12 standard deviations (Poisson) and a small margin;
+        0 when the layout would not fit u32 cursors."""
+        nparts = num_partitions_for(n, self.config.partition_size)
+        mean = n / nparts
+        cap = int(math.ceil(mean + 12.0 * math.sqrt(mean) + 16))
+        return cap if nparts * cap < 2**32 and cap < 65536 else 0
+
+    def _group_padded(self, dk: DeviceKeys, seed: int, nparts: int, cap: int, chunks):
+        """K3 into fixed-capacity slots (one launch per arriving chunk), counts
+        from the cursors, K2 layout. None if a partition overflowed."""
+        dev, B = self.device, self.bcount
+        n = dk.n
+        st = _native.stream()
+        P = _native.ptr
+        L = _native.lib()
+        cursor = torch.empty(nparts, dtype=torch.int32, device=dev)
+        lo = torch.empty(nparts * cap, dtype=torch.int64, device=dev)
+        bid = torch.empty(nparts * cap, dtype=torch.int16, device=dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        base = P(dk.keys64)
+        cur = torch.cuda.current_stream(dev)
+        for i, (a, b, ev) in enumerate(chunks or [(0, n, None)]):
+            if ev is not None:
+                cur.wait_event(ev)  # this chunk's host-to-device copy is done
+            _native.check(L.phb_scatter_padded(base + 8 * a, b - a, seed, nparts,
+                                               P(self.entries), B, cap, int(i == 0), P(cursor),
+                                               P(lo), P(bid), P(flag), st), "phb_scatter_padded")
+        counts = torch.empty(nparts, dtype=torch.int32, device=dev)
+        _native.check(L.phb_padded_counts(P(cursor), nparts, cap, P(counts), P(flag), st),
+                      "phb_padded_counts")
+        key_off = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+        deltas = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
+        stats = torch.empty(3, dtype=torch.int64, device=dev)
+        _native.check(L.phb_layout(P(counts), nparts, 0, 0, n, nparts, P(key_off), P(deltas),
+                                   P(stats), st), "phb_layout")
+        stats[2:3].copy_(flag)
+        self._pinned3.copy_(stats, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        if int(self._pinned3[2]):
+            return None  # a partition exceeded its slots: use the counted layout
+        return lo, bid, key_off, deltas, stats[:2], int(self._pinned3[1])
+
+    def run(self, dk: DeviceKeys, seed: int, instrument: bool = False,
+            chunks=None) -> DeviceBuild | tuple[int, int]:
         """One attempt. Returns DeviceBuild, or (first_bad, code) on failure.
         instrument: also keep per-bucket trials, per-partition trials and the
-        (partition, bucket) key counts (analysis.measure_work)."""
+        (partition, bucket) key counts (analysis.measure_work).
+        chunks: [(begin, end, cuda event)] of u64 keys still being copied to
+        the device; the grouping pass consumes each chunk once it has landed."""
         cfg, dev, B = self.config, self.device, self.bcount
         n = dk.n
         nparts = num_partitions_for(n, cfg.partition_size)
@@ -137,7 +185,32 @@ class BuildEngine:
         k64 = P(dk.keys64) if dk.is_u64 else None
         buf = None if dk.is_u64 else P(dk.buf)
         offs = None if dk.is_u64 else P(dk.offsets)
-        launches = 0
+
+        # u64 keys still arriving from the host: fixed-capacity grouping, no
+        # counting pass, each chunk grouped as soon as it lands (the copy and
+        # the grouping overlap). Keys already in HBM, byte keys, or an
+        # overflow: count, lay out, scatter (the counted pair is 0.25 ms faster
+        # than the fixed-capacity pass when there is no copy to hide).
+        grouped = None
+        cap = self.padded_capacity(n) if chunks and dk.is_u64 and not instrument else 0
+        if cap and k64 % 16 == 0:
+            grouped = self._group_padded(dk, seed, nparts, cap, chunks)
+        elif chunks:
+            for _, _, ev in chunks:
+                torch.cuda.current_stream(dev).wait_event(ev)
+        if grouped is not None:
+            lo, bid, key_off, deltas, stats, m_max = grouped
+            seeds = torch.zeros(B * nparts, dtype=torch.int64, device=dev)
+            part_trials = torch.empty(nparts, dtype=torch.int64, device=dev)
+            status = torch.empty(nparts, dtype=torch.uint8, device=dev)
+            glo = torch.empty(nparts * cap, dtype=torch.int64, device=dev)
+            queue = torch.empty(1, dtype=torch.int32, device=dev)
+            _native.check(L.phb_search_strided(P(lo), P(bid), P(key_off), 0, nparts, 0, B,
+                                               cfg.seed_cap, cfg.tie_desc, m_max, P(seeds), 1,
+                                               nparts, None, P(part_trials), P(status), P(glo),
+                                               P(queue), cap, st), "phb_search_strided")
+            return self._encode(n, nparts, seed, key_off, deltas, stats, seeds, status,
+                                part_trials)
 
         counts = torch.zeros(nparts, dtype=torch.int32, device=dev)
         _native.check(L.phb_hash_count(buf, offs, k64, n, seed, nparts, P(counts), st),
@@ -173,6 +246,16 @@ class BuildEngine:
                                    P(trials) if instrument else None,
                                    P(part_trials), P(status), P(glo), P(queue), st),
                       "phb_search")
+        return self._encode(n, nparts, seed, key_off, deltas, stats, seeds, status, part_trials,
+                            trials, part_trials if instrument else None, sizes)
+
+    def _encode(self, n, nparts, seed, key_off, deltas, stats, seeds, status, part_trials,
+                trials=None, keep_part_trials=None, sizes=None):
+        """K5: plan (status / trials reduction, sizes) and the serialized body."""
+        dev, B = self.device, self.bcount
+        st = _native.stream()
+        P = _native.ptr
+        L = _native.lib()
         ws = torch.empty(int(L.phb_encode_workspace_bytes(nparts, B, self.mono)),
                          dtype=torch.uint8, device=dev)
         summ = self._summary
@@ -188,8 +271,7 @@ class BuildEngine:
                                          nparts, P(stats), P(ws), P(blob), blob.numel(), st),
                       "phb_encode_write")
         return DeviceBuild(n, nparts, B, seed, key_off, deltas, seeds, blob, total,
-                           int(summ[1]), int(summ[2]), trials,
-                           part_trials if instrument else None, sizes)
+                           int(summ[1]), int(summ[2]), trials, keep_part_trials, sizes)
 
 
 class Mphf:
@@ -438,14 +520,15 @@ def build(keys, config: BuildConfig | None = None) -> Mphf:
         raise InvalidConfig("need at least one key")
     dev = _native.require_device()
     t0 = time.perf_counter()
-    dk = to_device(keys, dev)
+    dk, chunks = to_device_chunked(keys, dev)
     if dk.n < 1:
         raise InvalidConfig("need at least one key")
     engine = BuildEngine(config, dev)
     last: str | None = None
     for attempt in range(MAX_ATTEMPTS):
         seed = config.global_seed + attempt
-        res = engine.run(dk, seed)
+        res = engine.run(dk, seed, chunks=chunks)
+        chunks = None  # a retry finds every key on the device
         if isinstance(res, tuple):
             bad, code = res
             reason = "unseparable duplicate hashes" if code == 1 else "seed cap hit"

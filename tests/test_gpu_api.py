@@ -324,3 +324,29 @@ def test_random_string_configs_vs_oracle(phb, orc, case):
     ref = orc.build((corpus.buf, corpus.offsets), lambda_=lam, P=P, encoder=enc)
     assert f.serialize() == ref.serialize(), (lam, P, enc, n)
     assert f.is_bijection_on(corpus)
+
+
+def test_pinned_chunked_build_equals_device_build(phb):
+    """Pinned host keys (> one 8M-key chunk) take the overlapped path: chunked
+    copies on a side stream, fixed-capacity grouping per landed chunk, strided
+    search. Bytes equal the counted path's (keys already in HBM), also when a
+    forced overflow sends the build back to the counted layout."""
+    from paper_2404_18497_b200.keygen import synth_u64_device, to_device_chunked
+    from paper_2404_18497_b200.mphf import BuildEngine
+
+    n = 20_000_001
+    dev_keys = synth_u64_device(n, 5)
+    host = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    host.copy_(dev_keys)
+    cfg = phb.BuildConfig(lambda_=8.0, partition_size=2500.0, encoder="ic-r")
+    want = phb.build(dev_keys, cfg).serialize()
+    assert phb.build(host, cfg).serialize() == want
+    # forced overflow: 100 slots per partition cannot hold ~2500 keys
+    eng = BuildEngine(cfg)
+    eng.padded_capacity = lambda n: 100
+    dk, chunks = to_device_chunked(host, dev_keys.device)
+    assert chunks and len(chunks) == 3
+    res = eng.run(dk, 0, chunks=chunks)
+    torch.cuda.synchronize()
+    ref = BuildEngine(cfg).run(phb.keygen.to_device(dev_keys, dev_keys.device), 0)
+    assert torch.equal(res.blob[57:res.total_bytes], ref.blob[57:ref.total_bytes])
