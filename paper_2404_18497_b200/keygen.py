@@ -133,10 +133,16 @@ def staged_h2d(host: np.ndarray, device: torch.device, pad: int = 0) -> torch.Te
 
 
 def _staged_copy(src: np.ndarray, out: torch.Tensor, nbytes: int, device) -> None:
+    for _ in _staged_chunks(src, out, nbytes, device, torch.cuda.current_stream(device)):
+        pass
+
+
+def _staged_chunks(src: np.ndarray, out: torch.Tensor, nbytes: int, device, stream):
+    """Generator: per staging chunk, the threaded host copy into a pinned slot
+    and the DMA into out on `stream`; yields (byte begin, byte end, event)."""
     st = _stage_init()
     pool = st["pool"]
     workers = pool._max_workers
-    stream = torch.cuda.current_stream(device)
     for k, a in enumerate(range(0, nbytes, _STAGE_BYTES)):
         b = min(a + _STAGE_BYTES, nbytes)
         slot = k % _STAGE_SLOTS
@@ -149,10 +155,12 @@ def _staged_copy(src: np.ndarray, out: torch.Tensor, nbytes: int, device) -> Non
                 for o in range(0, b - a, step)]
         for fu in futs:
             fu.result()
-        out[a:b].copy_(st["bufs"][slot][: b - a], non_blocking=True)
+        with torch.cuda.stream(stream):
+            out[a:b].copy_(st["bufs"][slot][: b - a], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(stream)
         st["events"][slot] = ev
+        yield a, b, ev
 
 
 _COPY_CHUNK_KEYS = 8 << 20  # 64 MB of u64 keys per chunk (even: 16-byte aligned chunk starts)
@@ -184,6 +192,30 @@ def to_device_chunked(keys, device: torch.device):
                 chunks.append((a, b, ev))
         out.record_stream(cs)
         return DeviceKeys(n, keys64=out, h2d_bytes=n * 8), chunks
+    host = None
+    if isinstance(keys, np.ndarray) and keys.dtype in (np.uint64, np.int64) and keys.ndim == 1:
+        host = np.ascontiguousarray(keys)
+    elif (isinstance(keys, torch.Tensor) and not keys.is_cuda and not keys.is_pinned()
+          and keys.dtype in (torch.int64, torch.uint64) and keys.dim() == 1):
+        host = keys.contiguous().view(torch.int64).numpy()
+    if host is not None and host.size > _COPY_CHUNK_KEYS:
+        # pageable keys: the staged copy runs chunk by chunk as the build pulls
+        # the chunks, so the host copy of chunk k+1 overlaps chunk k's DMA and
+        # grouping pass
+        n = host.size
+        out = torch.empty(n, dtype=torch.int64, device=device)
+        cs = _copy_streams.get(device)
+        if cs is None:
+            cs = _copy_streams[device] = torch.cuda.Stream(device)
+        cs.wait_stream(torch.cuda.current_stream(device))
+        out.record_stream(cs)
+
+        def chunks():
+            with _stage_lock:
+                src = host.view(np.uint8)
+                for a, b, ev in _staged_chunks(src, out.view(torch.uint8), n * 8, device, cs):
+                    yield a // 8, b // 8, ev
+        return DeviceKeys(n, keys64=out, h2d_bytes=n * 8), chunks()
     return to_device(keys, device), None
 
 
