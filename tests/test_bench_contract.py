@@ -21,3 +21,29 @@ def test_reference_arm_json_line():
     assert line["unit"] == "keys/s" and line["value"] > 0 and line["higher_is_better"]
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_json_line():
+    """bench.py's GPU arm on a small key count: every field of the driver's
+    contract plus the roofline / cpu_baseline / e2e objects."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--steps", "3", "--warmup", "3",
+                        "--keys", "4000000", "--e2e-steps", "1", "--ref-sample", "200000"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e",
+              "gpu_launches", "roofline", "clocks", "cpu_baseline", "query", "bits_per_key"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["value"] > 0
+    assert line["gpu_launches"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in line["roofline"], k
+    assert line["e2e"]["h2d_bytes_per_step"] == 4_000_000 * 8
+    assert line["query"]["bijection_verified"] and line["query"]["encoded"]["equal_to_matrix_query"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in line["cpu_baseline"], k
