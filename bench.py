@@ -1,31 +1,42 @@
 """PHOBIC construction benchmark (BASELINE.json configs[1]: C2).
 
-Workload: n = 100M distinct 64-bit keys (synthetic, mix64(offset + i)),
-lambda = 9, P = 2500, interleaved-compact encoding ("fast-query ~2.17
-bits/key" config), beta_eps assignment, global seed 0.
+Headline workload (C2): n = 100M distinct 64-bit keys per GPU (synthetic,
+mix64(rank*n + i)), lambda = 9, P = 2500, interleaved-compact encoding (the
+"fast-query ~2.17 bits/key" config), beta_eps assignment, global seed 0.
 
 One step = one full device build pass over the resident keys:
   murmur3 + partition histogram -> layout -> scatter by partition ->
   per-partition seed search -> interleaved encoding -> serialized body
-(all kernels of paper_2404_18497_b200, incl. the two host syncs of the
-pipeline). `value` is keys/s with keys already in HBM; `e2e` is the same
-metric through the public API `build(pinned_host_keys, cfg)` with the H2D
-copy of the keys and the D2H copy of the encoded structure inside the
-timed region.
+(all kernels of paper_2404_18497_b200, incl. the pipeline's host syncs).
+`value` is keys/s with keys already in HBM; `e2e` is the same metric through
+the public API `build(pinned_host_keys, cfg)` with the H2D copy of the keys
+and the D2H copy of the encoded structure inside the timed region.
 
-N > 1 (torchrun): one build over n = 100M x N keys, sharded 100M per rank and
-routed to partition owners with NCCL (weak scaling; distributed.py).
+N > 1: one process per GPU. Launched by the driver under torchrun, or, when
+WORLD_SIZE is unset, bench.py re-executes itself under torchrun with N ranks
+(--gpus N). Headline = one sharded build over 100M x N keys (weak scaling,
+records routed to partition owners, distributed.py); `c3_strong` = one
+sharded build of 1B keys in total over the N GPUs (strong scaling, BASELINE
+configs[2]).
 
---impl reference: the reference algorithm's CPU implementation (the oracle
-port, oracle/phobic_oracle.c, all host threads) on a bounded sample of the
-same workload.
+At N = 1 the line also carries `configs`: the other BASELINE configs measured
+in the same run under the same clock sampler (C1, the C4
+lambda sweep, C5 strings, and the paper-matched row: 100M strings of 10-50 B
+at lambda = 9 IC-C, on which vs_baseline is based).
+
+--impl reference: the reference's own CPU implementation, pilothash.build
+(installed offline into baseline/_ref by tools/install_reference.sh), on all
+host cores, on a bounded sample of the same key stream. If that install is
+absent, the oracle port (oracle/phobic_oracle.c) stands in and says so.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -38,15 +49,16 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "MPHF build ns/key (keys/s) at 1/2/4/8 B200 @ bits/key; GPU query Mq/s"
 N_KEYS = 100_000_000
+N_C3 = 1_000_000_000
 LAMBDA = 9.0
 PSIZE = 2500.0
 ENCODER = "ic-c"
-PUBLISHED_NS_PER_KEY = 28.0  # PHOBIC-GPU lambda=9 IC-C, RTX 3090
+PUBLISHED_NS_PER_KEY = 28.0  # PHOBIC-GPU lambda=9 IC-C, 100M strings 10-50 B, RTX 3090
 # SURVEY.md §8(d), per key: the grouping pass reads the key (8 B) and writes
 # (lo, bucket id) (10 B); the search reads the record (10 B)
 ALGO_BYTES = {"total": 28, "hash_count": 8, "scatter": 18, "group": 18, "search": 10}
-KERNELS_PER_BUILD = 12  # padded_init, scatter_padded, padded_counts, layout, search, 7 encode
-# (profiles/r1_launches_c2.csv: the ncu launch list of one build, plus two torch zero-fills)
+QUERY_BYTES = 16  # per query: the 8 B key read + the 8 B position written
+REF_DIR = ROOT / "baseline" / "_ref"
 
 
 def _peaks():
@@ -54,6 +66,13 @@ def _peaks():
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
     except Exception:
         return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def _json_or_none(p: Path):
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -113,12 +132,36 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# --------------------------------------------------------------------- ranks
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int, script: str | None = None) -> int:
+    """Re-execute this script (same arguments) under torchrun with n ranks,
+    one per GPU; returns the ranks' exit status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), script or str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")        # communicator init (NVLS / P2P) stays visible
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    print(f"bench.py: spawning {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
+
+
 def dist_init(n_gpus: int, backend: str = "nccl", same_device: bool = False):
     import torch
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
 
@@ -129,6 +172,7 @@ def dist_init(n_gpus: int, backend: str = "nccl", same_device: bool = False):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
+        assert dist.get_world_size() == n_gpus
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
@@ -152,8 +196,61 @@ def allmax(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_baseline(sample_keys: int, threads: int):
-    """The reference algorithm on the host (oracle port), bounded sample."""
+def allmin_flag(ok: bool, world: int) -> bool:
+    if world == 1:
+        return ok
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([1 if ok else 0], dtype=torch.int64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+# ------------------------------------------------------------ CPU reference
+def _ref_available() -> bool:
+    return (REF_DIR / "pilothash" / "__init__.py").exists()
+
+
+def _import_pilothash():
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/phb_numba_cache")
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import pilothash
+
+    return pilothash
+
+
+def reference_build(sample_keys: int, threads: int, offset: int = 0):
+    """One timed build of a bounded sample of the bench key stream by the
+    reference's own CPU implementation: pilothash.build (mphf.py:236-290) with
+    config.threads = all host cores (its thread pool, builder.py:260-271).
+    Keys are the u64 stream as 8-byte little-endian strings (the reference's
+    key ABI)."""
+    import numpy as np
+
+    from paper_2404_18497_b200.keygen import synth_u64
+
+    ph = _import_pilothash()
+    keys = synth_u64(sample_keys, offset)
+    corpus = ph.KeyCorpus(keys.view(np.uint8).copy(),
+                          np.arange(0, 8 * sample_keys + 1, 8, dtype=np.int64))
+    cfg = ph.BuildConfig(lambda_=LAMBDA, partition_size=PSIZE, encoder=ENCODER, threads=threads)
+    t0 = time.perf_counter()
+    f = ph.build(corpus, cfg)
+    dt = time.perf_counter() - t0
+    return {"value": sample_keys / dt, "unit": "keys/s", "cores": threads, "kind": "reference",
+            "impl": "pilothash 0.1.0 build() (numba kernels), baseline/_ref",
+            "trials_per_s": f.stats.trials_total / dt,
+            "sample": f"{sample_keys:,} keys of the same synthetic stream (8-byte LE strings), "
+                      f"lambda=9 P=2500 IC-C, pilothash.build(threads={threads}) in {dt:.2f} s",
+            "ns_per_key": dt * 1e9 / sample_keys, "bits_per_key": f.bits_per_key()}
+
+
+def port_build(sample_keys: int, threads: int):
+    """The oracle port (C restatement of the reference, oracle/) on the host."""
+    import numpy as np
+
     from oracle import oracle
     from paper_2404_18497_b200.keygen import synth_u64
 
@@ -163,14 +260,29 @@ def cpu_baseline(sample_keys: int, threads: int):
     f = oracle.build(keys, lambda_=LAMBDA, P=PSIZE, encoder=ENCODER, threads=threads)
     body = f.body()
     dt = time.perf_counter() - t0
-    import numpy as np
-
     trials = int(np.asarray(f.trials).sum())
     return {"value": sample_keys / dt, "unit": "keys/s", "cores": threads, "kind": "port",
+            "impl": "oracle/phobic_oracle.c (C restatement of the reference)",
             "trials_per_s": trials / dt,
             "sample": f"{sample_keys:,} keys of the same synthetic stream, lambda=9 IC-C, "
                       f"full build (hash, partition, search, encode) in {dt:.2f} s",
-            "ns_per_key": dt * 1e9 / sample_keys, "bits_per_key": (len(body) + 57 + 8 - 16) * 8 / sample_keys}
+            "ns_per_key": dt * 1e9 / sample_keys,
+            "bits_per_key": (len(body) + 57 + 8 - 16) * 8 / sample_keys}
+
+
+def cpu_baseline(sample_keys: int, threads: int):
+    """The reference's CPU build on the host: pilothash itself when installed,
+    else the oracle port (kind says which)."""
+    if _ref_available():
+        try:
+            return reference_build(sample_keys, threads)
+        except Exception as exc:  # fall back, loudly
+            r = port_build(sample_keys, threads)
+            r["note"] = f"pilothash unavailable ({type(exc).__name__}: {exc}); oracle port used"
+            return r
+    r = port_build(sample_keys, threads)
+    r["note"] = "baseline/_ref not installed (tools/install_reference.sh); oracle port used"
+    return r
 
 
 def run_reference(args):
@@ -178,12 +290,22 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    sample = args.ref_sample or max(200_000, min(4_000_000, 250_000 * threads))
-    vals = []
-    for i in range(args.warmup + args.steps):
+    total = args.warmup + args.steps
+    if args.ref_sample:
+        sample = args.ref_sample
+    else:
+        # size each step so the whole run stays within ~3 minutes: a small
+        # calibration build (also the numba JIT warm-up) measures the rate
+        cal = cpu_baseline(200_000, threads)
+        budget_s = 170.0 / max(total, 1)
+        sample = int(min(8_000_000, max(200_000, budget_s * cal["value"])))
+    vals, r = [], None
+    for i in range(total):
         r = cpu_baseline(sample, threads)
         if i >= args.warmup:
             vals.append(r["value"])
+    if not vals:
+        vals = [r["value"]]
     v = statistics.median(vals)
     line = {"metric": METRIC, "value": v, "unit": "keys/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample / v * 1e3,
@@ -191,19 +313,163 @@ def run_reference(args):
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"C2 sample: {sample:,} u64 keys, lambda=9, P=2500, IC-C",
                        "n_keys": sample, "lambda": LAMBDA, "partition_size": PSIZE,
-                       "encoder": ENCODER},
+                       "encoder": ENCODER, "same_config": False,
+                       "why_sample": "the full 100M-key C2 build takes ~6 min on the host; "
+                                     "each step is a bounded sample of the same key stream"},
             "cpu_baseline": {**r, "value": v},
             "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------- GPU arm
+def _event():
+    import torch
+
+    return torch.cuda.Event(enable_timing=True)
+
+
+def _timed(fn, reps: int):
+    """Device time per call (CUDA events on the current stream, synchronized
+    on both sides), and the last result."""
+    import torch
+
+    torch.cuda.synchronize()
+    e0, e1 = _event(), _event()
+    e0.record()
+    r = None
+    for _ in range(reps):
+        r = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, r
+
+
+def _string_keys(n: int, lo: int, hi: int, seed: int, dev):
+    """n random printable strings, lengths uniform in [lo, hi] (device RNG: input generation)."""
+    import torch
+
+    from paper_2404_18497_b200.keygen import DeviceKeys
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    lens = torch.randint(lo, hi + 1, (n,), generator=g, device=dev, dtype=torch.int64)
+    offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(lens, 0, out=offsets[1:])
+    total = int(offsets[-1].item())
+    buf = torch.randint(33, 127, (total,), generator=g, device=dev, dtype=torch.uint8)
+    return DeviceKeys(n, buf=buf, offsets=offsets), total
+
+
+def _config_row(name, dk, cfg, reps, extra=None):
+    """One BASELINE config on this GPU: device build time (keys resident),
+    bits/key, trials/key, batched query rate, bijection."""
+    import torch
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.mphf import BuildEngine
+
+    eng = BuildEngine(cfg)
+    res = eng.run(dk, 0)  # warm-up
+    ms, res = _timed(lambda: eng.run(dk, 0), reps)
+    assert not isinstance(res, tuple), f"{name}: build failed"
+    f = phb.Mphf._from_device(res, cfg, eng, None)
+    out = f.query_device(dk)
+    ok = f.verify_device(out)
+    q_ms, _ = _timed(lambda: f.query_device(dk), 3)
+    n = dk.n
+    row = {"config": name, "n": n, "lambda": cfg.lambda_, "encoder": cfg.encoder,
+           "build_ms": round(ms, 3), "ns_per_key": ms * 1e6 / n, "keys_per_s": n / (ms * 1e-3),
+           "bits_per_key": (res.total_bytes + 8 - 16) * 8 / n,
+           "trials_per_key": res.trials_total / n, "query_ms": round(q_ms, 3),
+           "query_Mq_s": n / (q_ms * 1e-3) / 1e6, "bijection": bool(ok), "reps": reps}
+    if extra:
+        row.update(extra)
+    del f, res, eng, out
+    torch.cuda.empty_cache()
+    return row
+
+
+def run_configs(dev, args):
+    """The other BASELINE configs on one GPU, same process, same clock sampler."""
+    import torch
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.keygen import DeviceKeys, synth_u64_device
+
+    rows = []
+    cfg = lambda lam, enc: phb.BuildConfig(lambda_=lam, partition_size=PSIZE, encoder=enc)
+    keys = synth_u64_device(1_000_000, 0)
+    rows.append(_config_row("C1: 1M u64, lambda=5, IC-C", DeviceKeys(1_000_000, keys64=keys),
+                            cfg(5.0, "ic-c"), 10))
+    keys = synth_u64_device(args.n, 0)
+    dk = DeviceKeys(args.n, keys64=keys)
+    for lam in (4.0, 5.0, 6.0, 7.0, 8.0, 9.0):
+        rows.append(_config_row(f"C4: {args.n / 1e6:g}M u64, lambda={lam:g}, IC-R", dk,
+                                cfg(lam, "ic-r"), 3))
+    del keys, dk
+    torch.cuda.empty_cache()
+    dk, total = _string_keys(args.n, 10, 100, 2024, dev)
+    rows.append(_config_row(f"C5: {args.n / 1e6:g}M strings of 10-100 B, lambda=8, IC-R", dk,
+                            cfg(8.0, "ic-r"), 3,
+                            {"mean_key_bytes": total / args.n, "key_bytes_total": total}))
+    del dk
+    torch.cuda.empty_cache()
+    dk, total = _string_keys(args.n, 10, 50, 2025, dev)
+    paper = _config_row(f"paper: {args.n / 1e6:g}M strings of 10-50 B, lambda=9, IC-C", dk,
+                        cfg(9.0, "ic-c"), 3,
+                        {"mean_key_bytes": total / args.n, "key_bytes_total": total,
+                         "published_ns_per_key": PUBLISHED_NS_PER_KEY,
+                         "published": "PHOBIC-GPU, RTX 3090 + 8 CPU threads, 2.17 bits/key "
+                                      "(PAPER.md:282)"})
+    rows.append(paper)
+    del dk
+    torch.cuda.empty_cache()
+    return rows, paper  # C3 (1B keys) is c3_strong: at N = 1 the whole build on one GPU
+
+
+def run_c3_strong(args, rank, world, dops):
+    """BASELINE configs[2]: 1B keys in total, sharded over the N ranks
+    (strong scaling); N = 1 is the whole 1B-key build on one GPU."""
+    import torch
+
+    import paper_2404_18497_b200 as phb
+    from paper_2404_18497_b200.keygen import DeviceKeys, synth_u64_device
+    from paper_2404_18497_b200.mphf import BuildEngine
+
+    n_all = N_C3
+    lo = rank * n_all // world
+    hi = (rank + 1) * n_all // world
+    keys = synth_u64_device(hi - lo, lo)
+    dk = DeviceKeys(hi - lo, keys64=keys)
+    cfg = phb.BuildConfig(lambda_=LAMBDA, partition_size=PSIZE, encoder=ENCODER)
+    if world > 1:
+        from paper_2404_18497_b200.distributed import build_distributed
+
+        step = lambda: build_distributed(dk, cfg, ops=dops, to_host=False,
+                                         transport=args.transport)
+    else:
+        eng = BuildEngine(cfg)
+        step = lambda: eng.run(dk, 0)
+    res = step()
+    barrier(world)
+    ms, res = _timed(step, 2)
+    ms = allmax(ms, world)
+    assert not isinstance(res, tuple), "C3 build failed"
+    bits = (res.total_bytes + 8 - 16) * 8 / n_all
+    del keys, dk, res
+    torch.cuda.empty_cache()
+    return {"n_keys_total": n_all, "n_gpus": world, "ms": ms, "keys_per_s": n_all / (ms * 1e-3),
+            "ns_per_key": ms * 1e6 / n_all, "bits_per_key": bits, "scaling": "strong"}
+
+
 def run_gpu(args):
+    import numpy as np
     import torch
 
     import paper_2404_18497_b200 as phb
     from paper_2404_18497_b200 import _native
     from paper_2404_18497_b200.keygen import synth_u64_device, to_device
-    from paper_2404_18497_b200.mphf import BuildEngine
+    from paper_2404_18497_b200.mphf import BuildEngine, HEADER_FIXED
 
     rank, world, local = dist_init(args.gpus, args.backend, args.same_device)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -213,18 +479,17 @@ def run_gpu(args):
     dk = to_device(keys, dev)
     eng = BuildEngine(cfg, dev)
 
-    # per-kernel events around the pipeline's native calls (search timing)
+    # per-kernel events around the pipeline's native calls (stage timing)
     L = _native.lib()
     stage = {}
     wrapped = {}
     for name in ("phb_hash_count", "phb_scatter", "phb_search", "phb_scatter_padded",
-                 "phb_search_strided"):
+                 "phb_search_strided", "phb_scatter_p2p"):
         fn = getattr(L, name)
 
         def mk(fn, name):
             def w(*a):
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
+                e0, e1 = _event(), _event()
                 e0.record()
                 rc = fn(*a)
                 e1.record()
@@ -235,6 +500,7 @@ def run_gpu(args):
         wrapped[name] = fn
         setattr(L, name, mk(fn, name))
 
+    dops = None
     if world > 1:
         from paper_2404_18497_b200.distributed import DeviceOps, build_distributed
 
@@ -253,14 +519,15 @@ def run_gpu(args):
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
+    start, end = _event(), _event()
     with ClockSampler(local) as clk:
+        launches0 = _native.launch_count()
         start.record()
         for _ in range(args.steps):
             res = step()
         end.record()
         torch.cuda.synchronize()
+        launches = _native.launch_count() - launches0
     barrier(world)
     torch.cuda.synchronize()
     ms = start.elapsed_time(end) / args.steps
@@ -272,6 +539,10 @@ def run_gpu(args):
     total_keys = n * world
     bits = (res.total_bytes + 8 - 16) * 8 / total_keys
     value = total_keys / (ms * 1e-3)
+    timed_body = res.blob[HEADER_FIXED:res.total_bytes].cpu().numpy()
+    timed_trials = res.trials_total
+    del res
+    torch.cuda.empty_cache()
 
     # ---- e2e through the public API: pinned host keys -> Mphf (host bytes)
     host = torch.empty(n, dtype=torch.int64, pin_memory=True)
@@ -280,11 +551,12 @@ def run_gpu(args):
     torch.cuda.empty_cache()
     e2e_ms = []
     blob_bytes = 0
+    f = None
     for i in range(1 + args.e2e_steps):
+        f = None
         torch.cuda.synchronize()
         barrier(world)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = _event(), _event()
         e0.record()
         if world > 1:
             f = build_distributed(host, cfg, ops=dops, transport=args.transport)
@@ -295,12 +567,15 @@ def run_gpu(args):
         blob_bytes = len(f._body)
         if i > 0:
             e2e_ms.append(e0.elapsed_time(e1))
-        del f
     e2e = allmax(statistics.median(e2e_ms) if e2e_ms else float("nan"), world)
+    # the timed device build and the public-API build produced the same structure
+    body_equal = bool(np.array_equal(np.asarray(f._body)[HEADER_FIXED:], timed_body)
+                      and f.stats.trials_total == timed_trials)
+    body_equal = allmin_flag(body_equal, world)
+    assert body_equal, "timed device build differs from the public-API build"
+    digest = hashlib.blake2b(bytes(f._body), digest_size=8).hexdigest()
 
-    # ---- batched GPU query of all n keys (Mq/s), from the last build
-    f = (build_distributed(host, cfg, ops=dops, transport=args.transport) if world > 1
-         else phb.build(host, cfg))
+    # ---- batched GPU query of all keys of this rank (Mq/s) on the e2e structure
     qkeys = host.to(dev)
     qdk = to_device(qkeys, dev)
     out = f.query_device(qdk)
@@ -308,61 +583,84 @@ def run_gpu(args):
         assert f.verify_device(out), "not a bijection"
     else:  # each rank checks its shard's outputs are distinct and in range
         assert bool(((out >= 0) & (out < f.n)).all()) and out.unique().numel() == out.numel()
-    torch.cuda.synchronize()
+
     def time_query(fn, reps=5):
         """median of per-call device times (CUDA events around each call)"""
-        ts = []
+        ts, r = [], None
         for _ in range(reps):
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            r = fn(qdk)
-            e1.record()
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
+            t, r = _timed(lambda: fn(qdk), 1)
+            ts.append(t)
         return statistics.median(ts), r
 
-    q_ms, out = time_query(f.query_device)
-    # the same batched query reading the seeds from the encoded section (K7e)
+    q_ms, out2 = time_query(f.query_device)
     qe_ms, oute = time_query(f.query_encoded_device)
-    enc_ok = bool(torch.equal(oute, out))
+    enc_ok = bool(torch.equal(oute, out2))
+    del out, out2, oute
+
+    # ---- multi-GPU: the sharded body equals a single-GPU build of all keys
+    parity = None
+    if world > 1 and args.check_parity:
+        other = "nccl" if args.transport == "p2p" else "p2p"
+        f2 = build_distributed(host, cfg, ops=dops, transport=other)
+        t_eq = bytes(f2._body) == bytes(f._body)
+        del f2
+        single_eq = None
+        if rank == 0:
+            allk = synth_u64_device(n * world, 0)
+            db = BuildEngine(cfg, dev).run(to_device(allk, dev), 0)
+            single_eq = bool(np.array_equal(db.blob[HEADER_FIXED:db.total_bytes].cpu().numpy(),
+                                            np.asarray(f._body)[HEADER_FIXED:]))
+            del allk, db
+            torch.cuda.empty_cache()
+        parity = {"transports_equal": allmin_flag(t_eq, world),
+                  "body_equal_single_gpu_build": single_eq,
+                  "what": f"body of the {world}-rank build ({args.transport}) vs the other "
+                          f"transport ({other}) and vs one GPU building all {n * world:,} keys"}
+        assert parity["transports_equal"] and (rank != 0 or single_eq), parity
+    del f
+    torch.cuda.empty_cache()
 
     peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    # the single-GPU build groups into fixed-capacity slots and searches them
-    # strided; the multi-GPU path uses the counted kernels
     if "phb_search_strided" in per:
         per["phb_search"] = per.pop("phb_search_strided")
     s_ms = per.get("phb_search", float("nan"))
-    achieved = n * ALGO_BYTES["search"] / (s_ms * 1e-3) / 1e9
+    n_local = n
+    achieved = n_local * ALGO_BYTES["search"] / (s_ms * 1e-3) / 1e9
     passes = {}
     for k, nm in (("phb_hash_count", "hash_count"), ("phb_scatter", "scatter"),
-                  ("phb_scatter_padded", "group")):
+                  ("phb_scatter_padded", "group"), ("phb_scatter_p2p", "scatter")):
         if k in per:
-            gbs = n * ALGO_BYTES[nm] / (per[k] * 1e-3) / 1e9
+            gbs = n_local * ALGO_BYTES[nm] / (per[k] * 1e-3) / 1e9
             passes[nm] = {"ms": round(per[k], 4), "GB/s": round(gbs, 1), "frac": round(gbs / hbm, 4)}
     passes["search"] = {"ms": round(s_ms, 4), "share_of_step": round(s_ms / ms, 4)}
-    traffic = None
-    tp = ROOT / "profiles" / "search_traffic_c2.json"
-    if tp.exists():
-        try:
-            traffic = json.loads(tp.read_text()).get("bytes_per_launch")
-        except Exception:
-            traffic = None
-    sm = None
-    sp = ROOT / "profiles" / "search_sm_c2.json"
-    if sp.exists():
-        try:
-            sm = json.loads(sp.read_text())
-        except Exception:
-            sm = None
+    straffic = _json_or_none(ROOT / "profiles" / "search_traffic_c2.json") or {}
+    sm = _json_or_none(ROOT / "profiles" / "search_sm_c2.json")
+    qprof = _json_or_none(ROOT / "profiles" / "query_c2.json") or {}
     clocks = clk.summary()
+    trials_per_key = timed_trials / total_keys
+    # issue-side roofline of k_search: the bit-parallel floor is one 32-bit
+    # word op (shared load + funnel shift + OR = 3 warp instructions per
+    # 32 lanes x 32 candidates) per 1024 of the reference's trials
+    floor_instr = trials_per_key / 1024.0 * 3.0
+    issue = None
+    if sm is not None:
+        ipk = sm["warp_instructions"] / sm.get("n_keys", 1e8)
+        issue = {"issue_active_pct": round(sm["issue_active_pct"], 1),
+                 "alu_pipe_pct": round(sm["alu_pipe_pct_elapsed"], 1),
+                 "shared_lsu_pct": round(sm["lsu_shared_wavefront_pct_elapsed"], 1),
+                 "warp_instructions_per_key": round(ipk, 1),
+                 "floor_instructions_per_key": round(floor_instr, 1),
+                 "frac": round(floor_instr / ipk * sm["issue_active_pct"] / 100.0, 4),
+                 "what": "instruction floor / measured instructions x issue-active "
+                         "(ncu --set full of the same workload)",
+                 "source": "profiles/search_sm_c2.json"}
+    q_gbs = n_local * QUERY_BYTES / (q_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": value / (1e9 / PUBLISHED_NS_PER_KEY),
+        "vs_baseline": None,
         "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"C2: n={n / 1e6:g}M u64 keys/GPU, lambda=9, P=2500, IC-C "
                                "(fast-query)",
@@ -374,34 +672,40 @@ def run_gpu(args):
                                    f"owners ({args.transport})" if world > 1 else "1 GPU")},
         "ns_per_key": ms * 1e6 / total_keys,
         "bits_per_key": bits,
+        "body_blake2b8": digest,
+        "timed_build_equals_e2e_build": body_equal,
         # the reference's work unit (one key x one (s, d) candidate, _kernels.py:236-240)
-        "search_work": {"trials_per_key": res.trials_total / total_keys,
-                        "trials_per_s": res.trials_total / (ms * 1e-3),
-                        "search_trials_per_s": (res.trials_total / (per["phb_search"] * 1e-3)
-                                                if "phb_search" in per else None)},
+        "search_work": {"trials_per_key": trials_per_key,
+                        "trials_per_s": timed_trials / (ms * 1e-3),
+                        "search_trials_per_s": (timed_trials / world / (s_ms * 1e-3)
+                                                if s_ms == s_ms else None)},
         "query": {"value": total_keys / (allmax(q_ms, world) * 1e-3) / 1e6, "unit": "Mq/s",
                   "ms": q_ms, "bijection_verified": True,
                   "what": "batched GPU query of every key (hash fused), keys resident",
+                  "roofline": {"bound": "hbm", "achieved": q_gbs, "peak": hbm, "unit": "GB/s",
+                               "frac": q_gbs / hbm,
+                               "algorithmic_bytes_per_query": QUERY_BYTES,
+                               "traffic": qprof.get("dram_bytes_per_query"),
+                               "source": "profiles/query_c2.json" if qprof else None},
                   "encoded": {"value": total_keys / (allmax(qe_ms, world) * 1e-3) / 1e6,
                               "unit": "Mq/s", "ms": qe_ms, "equal_to_matrix_query": enc_ok,
                               "what": "same query reading seeds from the encoded section"}},
         "e2e": {"value": total_keys / (e2e * 1e-3), "unit": "keys/s", "ms": e2e,
                 "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": blob_bytes,
-                "api": "paper_2404_18497_b200.build(pinned host uint64 tensor, BuildConfig)"},
-        "gpu_launches": KERNELS_PER_BUILD * args.steps,
-        "roofline": {"bound": "hbm", "kernel": "k_search", "achieved": achieved, "peak": hbm,
-                     "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "note": "search is issue/latency bound (integer + shared-memory bit "
-                             "ops), not HBM bound; algorithmic bytes = 10 B/key read "
-                             "(SURVEY.md §8(d)); see passes for the HBM-bound kernels",
+                "api": ("paper_2404_18497_b200.build(pinned host uint64 tensor, BuildConfig)"
+                        if world == 1 else "build_distributed(pinned host shard, BuildConfig)")},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "roofline": {"bound": "issue", "kernel": "k_search", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": straffic.get("bytes_per_launch"),
+                     "note": "k_search is bound by SM issue (integer ALU + shared-memory "
+                             "bit ops), not by HBM or tensor cores; achieved/peak/frac are "
+                             "its algorithmic 10 B/key against HBM as the contract asks, "
+                             "`issue` is the bound that applies; passes = the HBM-bound "
+                             "kernels",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "when" in peaks else "fallback",
-                     # the bound that does apply to k_search (ncu --set full, same workload)
-                     "sm": None if sm is None else {
-                         "issue_active_pct": round(sm["issue_active_pct"], 1),
-                         "alu_pipe_pct": round(sm["alu_pipe_pct_elapsed"], 1),
-                         "shared_lsu_pct": round(sm["lsu_shared_wavefront_pct_elapsed"], 1),
-                         "warp_instructions_per_key": round(sm["warp_instructions"] / 1e8, 1),
-                         "source": "profiles/search_sm_c2.json"}},
+                     "issue": issue},
         "passes": passes,
         # whole-build floor = 28 B/key of algorithmic traffic at peak HBM
         "build_roofline": {"algorithmic_bytes_per_key": ALGO_BYTES["total"],
@@ -409,15 +713,32 @@ def run_gpu(args):
                            "frac": (n * ALGO_BYTES["total"] / (hbm * 1e9) * 1e3) / ms},
         "clocks": clocks,
     }
+    if parity is not None:
+        line["multi_gpu_parity"] = parity
+    if not args.no_c3:
+        with ClockSampler(local) as clk3:
+            line["c3_strong"] = run_c3_strong(args, rank, world, dops)
+        line["c3_strong"]["clocks"] = clk3.summary()
+    if world == 1 and not args.no_configs:
+        with ClockSampler(local) as clkc:
+            rows, paper = run_configs(dev, args)
+        line["configs"] = {"rows": rows, "clocks": clkc.summary()}
+        # vs_baseline: the paper's PHOBIC-GPU figure is for 100M strings of
+        # 10-50 B at lambda = 9 IC-C, so it is compared with that row
+        line["vs_baseline"] = paper["keys_per_s"] / (1e9 / PUBLISHED_NS_PER_KEY)
+        line["vs_baseline_basis"] = ("configs 'paper' row (100M strings 10-50 B, lambda=9, "
+                                     "IC-C) / PHOBIC-GPU 28 ns/key (PAPER.md:282)")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        sample = args.ref_sample or max(200_000, min(4_000_000, 250_000 * threads))
+        sample = args.ref_sample or 4_000_000
         line["cpu_baseline"] = cpu_baseline(sample, threads)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
+        if dops is not None:
+            dops.close()
         dist.destroy_process_group()
 
 
@@ -431,6 +752,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs")
+    ap.add_argument("--no-c3", action="store_true", help="skip the 1B-key c3_strong build")
+    ap.add_argument("--check-parity", action=argparse.BooleanOptionalAction, default=True,
+                    help="N>1: compare bodies across transports and with a 1-GPU build")
     ap.add_argument("--backend", default="nccl", help="nccl (default) or gloo (validation)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 record routing: fused CUDA-IPC peer scatter (default) or NCCL "
@@ -440,8 +765,10 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_gpu(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    run_gpu(args)
 
 
 if __name__ == "__main__":

@@ -36,6 +36,9 @@ extern "C" {
 const char* phb_version(void);
 const char* phb_error_string(int code);
 int phb_device_sms(void);
+/* Kernel launches this library has issued in this process (all entry
+ * points; relaxed atomic counter). Host-only, no CUDA context needed. */
+unsigned long long phb_launch_count(void);
 
 /* ---------------------------------------------------------------------
  * Reference-shaped operators: one-for-one replacements of the three

@@ -65,6 +65,7 @@ OTHER = {
     "phb_version": ([], ctypes.c_char_p),
     "phb_error_string": ([INT], ctypes.c_char_p),
     "phb_encode_workspace_bytes": ([I64, I32, I32], SZ),
+    "phb_launch_count": ([], ctypes.c_ulonglong),
 }
 
 _lib = None
@@ -123,6 +124,11 @@ def ptr(t) -> int | None:
 
 def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libphobic_b200.so so far in this process."""
+    return int(load().phb_launch_count())
 
 
 def call(name: str, *args) -> None:

@@ -42,17 +42,38 @@ def murmur3_many(buf, offsets, seed, out_hi, out_lo) -> None:
 
 def build_partition_range(his, los, key_off, p_lo, p_hi, entries, bcount, seed_cap, tie_desc,
                           seeds_out, trials_out, status_out) -> None:
-    """_kernels.py:221-371 (outputs written in place, like the reference)."""
-    h, l, k = _dev(his), _dev(los), _dev(np.asarray(key_off, np.int64))
+    """_kernels.py:221-371 (outputs written in place, like the reference).
+
+    Only the rows this call owns are staged and written back: keys
+    [key_off[p_lo], key_off[p_hi]) go up, seeds / trials rows [p_lo, p_hi)
+    and status[p_lo:p_hi] come back. builder.build_all_partitions
+    (builder.py:260-271) calls this concurrently from a thread pool with
+    disjoint partition ranges over shared output arrays; the native call and
+    the copies release the GIL, so writing back whole arrays would clobber
+    the other threads' rows."""
+    p_lo, p_hi, bcount = int(p_lo), int(p_hi), int(bcount)
+    if p_hi <= p_lo:
+        return
+    key_off = np.asarray(key_off, np.int64)
+    k0, k1 = int(key_off[p_lo]), int(key_off[p_hi])
+    dev = _native.require_device()
+    ko = _dev(key_off)
+    h = _dev(np.asarray(his[k0:k1] if k1 > k0 else np.zeros(1, np.uint64)))
+    l = _dev(np.asarray(los[k0:k1] if k1 > k0 else np.zeros(1, np.uint64)))
     e = _dev(np.asarray(entries, np.float64))
-    s, t, st = _dev(seeds_out), _dev(trials_out), _dev(status_out)
-    _native.call("phb_build_partition_range", _native.ptr(h), _native.ptr(l), _native.ptr(k),
-                 int(p_lo), int(p_hi), _native.ptr(e), int(bcount), int(seed_cap),
-                 int(bool(tie_desc)), _native.ptr(s), _native.ptr(t), _native.ptr(st),
-                 _native.stream())
-    seeds_out[:] = s.cpu().numpy().view(np.uint64)
-    trials_out[:] = t.cpu().numpy()
-    status_out[:] = st.cpu().numpy()
+    rows = p_hi - p_lo
+    s = torch.zeros(rows * bcount, dtype=torch.int64, device=dev)
+    t = torch.zeros(rows * bcount, dtype=torch.int64, device=dev)
+    st = torch.zeros(rows, dtype=torch.uint8, device=dev)
+    # the C-ABI indexes keys by key_off and outputs by partition j: shift the
+    # base pointers so that index k0 / row p_lo land on element 0
+    _native.call("phb_build_partition_range", _native.ptr(h) - 8 * k0, _native.ptr(l) - 8 * k0,
+                 _native.ptr(ko), p_lo, p_hi, _native.ptr(e), bcount, int(seed_cap),
+                 int(bool(tie_desc)), _native.ptr(s) - 8 * p_lo * bcount,
+                 _native.ptr(t) - 8 * p_lo * bcount, _native.ptr(st) - p_lo, _native.stream())
+    seeds_out[p_lo * bcount:p_hi * bcount] = s.cpu().numpy().view(np.uint64)
+    trials_out[p_lo * bcount:p_hi * bcount] = t.cpu().numpy()
+    status_out[p_lo:p_hi] = st.cpu().numpy()
 
 
 def query_many_kernel(his, los, n, nparts, deltas, entries, bcount, seed_mat, out) -> None:

@@ -11,6 +11,8 @@
 
 namespace phb {
 
+unsigned long long g_launch_count = 0;
+
 int num_sms() {
   static int cached[64] = {0};
   int dev = 0;
@@ -83,6 +85,8 @@ const char* phb_error_string(int code) {
 }
 
 int phb_device_sms(void) { return num_sms(); }
+
+unsigned long long phb_launch_count(void) { return __atomic_load_n(&g_launch_count, __ATOMIC_RELAXED); }
 
 int phb_murmur3_many(const uint8_t* buf, const int64_t* offsets, int64_t n, uint64_t seed,
                      uint64_t* out_hi, uint64_t* out_lo, void* stream) {
@@ -214,7 +218,7 @@ int phb_build_partition_range(const uint64_t* his, const uint64_t* los, const in
   PHB_CUDA_TRY(cudaMallocAsync(&d_stat, 3 * sizeof(unsigned long long), st));
   PHB_CUDA_TRY(cudaMemsetAsync(d_stat, 0, 3 * sizeof(unsigned long long), st));
   int g = (int)std::min<int64_t>((p_hi - p_lo + 255) / 256, 1024);
-  k_range_max<<<g, 256, 0, st>>>(key_off, p_lo, p_hi, d_stat);
+  note_launch(), k_range_max<<<g, 256, 0, st>>>(key_off, p_lo, p_hi, d_stat);
   PHB_CUDA_TRY(cudaGetLastError());
   PHB_CUDA_TRY(cudaMemcpyAsync(h_stat, d_stat, sizeof(h_stat), cudaMemcpyDeviceToHost, st));
   PHB_CUDA_TRY(cudaStreamSynchronize(st));
@@ -260,7 +264,7 @@ int phb_offsets_from_deltas(const int64_t* deltas, int64_t n, int64_t nparts, in
                             void* stream) {
   if (nparts < 1) return PHB_E_ARGS;
   int g = (int)std::min<int64_t>((nparts + 256) / 256, 4096);
-  k_offsets_from_deltas<<<g, 256, 0, S(stream)>>>(deltas, n, nparts, key_off);
+  note_launch(), k_offsets_from_deltas<<<g, 256, 0, S(stream)>>>(deltas, n, nparts, key_off);
   return (int)cudaGetLastError();
 }
 
@@ -480,7 +484,7 @@ int phb_synth_keys(uint64_t* out, int64_t n, uint64_t offset, void* stream) {
   if (n < 0) return PHB_E_ARGS;
   if (n == 0) return 0;
   int g = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16);
-  k_synth<<<g, 256, 0, S(stream)>>>(out, n, offset);
+  note_launch(), k_synth<<<g, 256, 0, S(stream)>>>(out, n, offset);
   return (int)cudaGetLastError();
 }
 

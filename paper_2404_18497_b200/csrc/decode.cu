@@ -203,15 +203,15 @@ int launch_decode(const uint8_t* blob, int64_t ncols, const int64_t* host_info, 
   const int64_t total = ncols * per_col;
   int g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
   if (g < 1) g = 1;
-  k_decode_fields<<<g, 256, 0, st>>>(blob, dcols, ncols, per_col, nparts, B, mono, seeds);
+  note_launch(), k_decode_fields<<<g, 256, 0, st>>>(blob, dcols, ncols, per_col, nparts, B, mono, seeds);
   PHB_CUDA_TRY(cudaGetLastError());
   if (any_rice) {
     PHB_CUDA_TRY(cudaMallocAsync(&csum, sizeof(unsigned long long) * ncols * nch, st));
     PHB_CUDA_TRY(cudaMallocAsync(&pos, sizeof(uint64_t) * ncols * per_col, st));
-    k_highs_chunks<<<(unsigned)(ncols * nch), DT, 0, st>>>(blob, dcols, nch, csum);
-    k_highs_scan<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(ncols, nch, csum);
-    k_highs_emit<<<(unsigned)(ncols * nch), DT, 0, st>>>(blob, dcols, nch, csum, per_col, pos);
-    k_highs_apply<<<g, 256, 0, st>>>(dcols, ncols, per_col, pos, nparts, B, mono, seeds);
+    note_launch(), k_highs_chunks<<<(unsigned)(ncols * nch), DT, 0, st>>>(blob, dcols, nch, csum);
+    note_launch(), k_highs_scan<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(ncols, nch, csum);
+    note_launch(), k_highs_emit<<<(unsigned)(ncols * nch), DT, 0, st>>>(blob, dcols, nch, csum, per_col, pos);
+    note_launch(), k_highs_apply<<<g, 256, 0, st>>>(dcols, ncols, per_col, pos, nparts, B, mono, seeds);
     PHB_CUDA_TRY(cudaGetLastError());
     PHB_CUDA_TRY(cudaFreeAsync(csum, st));
     PHB_CUDA_TRY(cudaFreeAsync(pos, st));

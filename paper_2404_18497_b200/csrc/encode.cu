@@ -425,14 +425,14 @@ int launch_encode_plan(const EncodeArgs& a, void* ws, EncodeSummary* host_sum, c
                                  cudaMemcpyDeviceToDevice, st));
   } else {
     PHB_CUDA_TRY(cudaMemsetAsync(L.colstat, 0, (size_t)ncols * 65 * 8, st));
-    k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.colstat);
+    note_launch(), k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.colstat);
     PHB_CUDA_TRY(cudaGetLastError());
   }
-  k_plan<<<1, 1024, 0, st>>>(a, L.colstat, L.info, L.sum);
+  note_launch(), k_plan<<<1, 1024, 0, st>>>(a, L.colstat, L.info, L.sum);
   PHB_CUDA_TRY(cudaGetLastError());
-  k_rice_chunks<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks);
+  note_launch(), k_rice_chunks<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks);
   PHB_CUDA_TRY(cudaGetLastError());
-  k_rice_chunk_scan<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(ncols, nch, L.chunks,
+  note_launch(), k_rice_chunk_scan<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(ncols, nch, L.chunks,
                                                                a.rice_totals_out);
   PHB_CUDA_TRY(cudaGetLastError());
   if (host_sum) {
@@ -454,17 +454,17 @@ int launch_encode_write(const EncodeArgs& a, void* ws, uint8_t* blob, size_t blo
   PHB_CUDA_TRY(cudaMemsetAsync(blob, 0, blob_bytes, st));
   uint32_t* words = reinterpret_cast<uint32_t*>(blob);
   if (a.write_headers) {
-    k_headers<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(a, L.info, L.sum, words);
+    note_launch(), k_headers<<<(unsigned)cdiv(ncols, 256), 256, 0, st>>>(a, L.info, L.sum, words);
     PHB_CUDA_TRY(cudaGetLastError());
   }
   int64_t nd = a.nparts_global + 1;
   if (a.deltas && a.write_headers) {
-    k_deltas<<<(unsigned)std::min<int64_t>(cdiv(nd, 256), 4096), 256, 0, st>>>(a.deltas, nd, L.sum,
+    note_launch(), k_deltas<<<(unsigned)std::min<int64_t>(cdiv(nd, 256), 4096), 256, 0, st>>>(a.deltas, nd, L.sum,
                                                                         words);
     PHB_CUDA_TRY(cudaGetLastError());
   }
   Cols cols{a.seeds, a.nparts, a.bcount, a.mono, a.row0 * (a.mono ? (int64_t)a.bcount : 1)};
-  k_payload<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks, a.rice_base,
+  note_launch(), k_payload<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.info, L.chunks, a.rice_base,
                                                     words);
   return (int)cudaGetLastError();
 }
@@ -478,7 +478,7 @@ int launch_encode_stats(const EncodeArgs& a, void* ws, unsigned long long* colst
   (void)ws;
   PHB_CUDA_TRY(cudaMemsetAsync(colstat_out, 0, (size_t)ncols * 65 * 8, st));
   Cols cols{a.seeds, a.nparts, a.bcount, a.mono, 0};
-  if (cnt > 0) k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, colstat_out);
+  if (cnt > 0) note_launch(), k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, colstat_out);
   return (int)cudaGetLastError();
 }
 

@@ -266,9 +266,9 @@ int launch_murmur(const uint8_t* buf, const int64_t* offsets, const uint64_t* ke
   if (n <= 0) return 0;
   int g = grid_for(n);
   if (keys64)
-    k_murmur<<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, hi, lo);
+    note_launch(), k_murmur<<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, hi, lo);
   else
-    k_murmur<<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, hi, lo);
+    note_launch(), k_murmur<<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, hi, lo);
   return (int)cudaGetLastError();
 }
 
@@ -288,7 +288,7 @@ int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
     int64_t need = ((n >> 2) + 1023) / 1024;
     int gb = (int)std::max<int64_t>(1, std::min<int64_t>(need, num_sms()));
-    k_hash_count_u64x4<<<gb, 1024, sh, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n,
+    note_launch(), k_hash_count_u64x4<<<gb, 1024, sh, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n,
                                             seed, nparts, counts);
     return (int)cudaGetLastError();
   }
@@ -297,15 +297,15 @@ int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t
     int gs = g < 2 * num_sms() ? g : 2 * num_sms();
     size_t sh = nparts * sizeof(uint32_t);
     if (keys64)
-      k_hash_count<U64Keys, true><<<gs, 256, sh, st>>>(U64Keys{keys64}, n, seed, nparts, counts);
+      note_launch(), k_hash_count<U64Keys, true><<<gs, 256, sh, st>>>(U64Keys{keys64}, n, seed, nparts, counts);
     else
-      k_hash_count<ByteKeys, true>
+      note_launch(), k_hash_count<ByteKeys, true>
           <<<gs, 256, sh, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, counts);
   } else {
     if (keys64)
-      k_hash_count<U64Keys, false><<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, counts);
+      note_launch(), k_hash_count<U64Keys, false><<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, counts);
     else
-      k_hash_count<ByteKeys, false>
+      note_launch(), k_hash_count<ByteKeys, false>
           <<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, counts);
   }
   return (int)cudaGetLastError();
@@ -317,19 +317,19 @@ int launch_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
                    cudaStream_t st) {
   if (n <= 0) return 0;
   if (n >= (int64_t(1) << 32)) return 1003;  // u32 cursors
-  k_cursor_init<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+  note_launch(), k_cursor_init<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
       key_off, (int64_t)nparts, cursor);
   PHB_CUDA_TRY(cudaGetLastError());
   int g = grid_for(n);
   if (keys64 && aligned16(keys64)) {
     int g4 = grid_for((n + 3) / 4);
-    k_scatter_u64x4<<<g4, 256, 0, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n, seed,
+    note_launch(), k_scatter_u64x4<<<g4, 256, 0, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n, seed,
                                         nparts, entries, bcount, cursor, lo_out, bid_out);
   } else if (keys64) {
-    k_scatter<<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, entries, bcount, cursor,
+    note_launch(), k_scatter<<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, entries, bcount, cursor,
                                  lo_out, bid_out);
   } else {
-    k_scatter<<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, entries, bcount,
+    note_launch(), k_scatter<<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, entries, bcount,
                                  cursor, lo_out, bid_out);
   }
   return (int)cudaGetLastError();
@@ -341,13 +341,13 @@ int launch_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, uint
                           uint32_t* overflow, cudaStream_t st) {
   if ((uint64_t)nparts * cap >= (uint64_t(1) << 32)) return 1003;  // u32 cursors
   if (init) {
-    k_padded_init<<<(int)std::min<uint64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+    note_launch(), k_padded_init<<<(int)std::min<uint64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
         (int64_t)nparts, cap, cursor);
     PHB_CUDA_TRY(cudaGetLastError());
   }
   if (n <= 0) return 0;
   if (!aligned16(keys64)) return 1003;
-  k_scatter_padded_u64x4<<<grid_for((n + 3) / 4), 256, 0, st>>>(
+  note_launch(), k_scatter_padded_u64x4<<<grid_for((n + 3) / 4), 256, 0, st>>>(
       reinterpret_cast<const ulonglong2*>(keys64), n, seed, nparts, entries, bcount, cap, cursor,
       lo_out, bid_out, overflow);
   return (int)cudaGetLastError();
@@ -355,7 +355,7 @@ int launch_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, uint
 
 int launch_padded_counts(const uint32_t* cursor, int64_t nparts, uint32_t cap, uint32_t* counts,
                          uint32_t* overflow, cudaStream_t st) {
-  k_padded_counts<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+  note_launch(), k_padded_counts<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
       cursor, nparts, cap, counts, overflow);
   return (int)cudaGetLastError();
 }
@@ -363,7 +363,7 @@ int launch_padded_counts(const uint32_t* cursor, int64_t nparts, uint32_t cap, u
 int launch_bucket_ids(const uint64_t* his, int64_t n, const double* entries, uint32_t bcount,
                       uint16_t* bid, cudaStream_t st) {
   if (n <= 0) return 0;
-  k_bucket_ids<<<grid_for(n), 256, 0, st>>>(his, n, entries, bcount, bid);
+  note_launch(), k_bucket_ids<<<grid_for(n), 256, 0, st>>>(his, n, entries, bcount, bid);
   return (int)cudaGetLastError();
 }
 

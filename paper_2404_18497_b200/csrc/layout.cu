@@ -89,7 +89,7 @@ int launch_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int6
                   int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                   int64_t* stats, void*, size_t, cudaStream_t st) {
   if (nparts < 1) return 1003;  // PHB_E_ARGS
-  k_layout<<<1, LT, 0, st>>>(counts, nparts, key_base, part_base, global_n, global_nparts,
+  note_launch(), k_layout<<<1, LT, 0, st>>>(counts, nparts, key_base, part_base, global_n, global_nparts,
                              key_off, deltas, stats);
   return (int)cudaGetLastError();
 }
@@ -181,12 +181,12 @@ int launch_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t*
   int64_t* scratch = nullptr;
   const size_t cells = (size_t)(G * np > 0 ? G * np : 1);
   PHB_CUDA_TRY(cudaMallocAsync(&scratch, 2 * cells * sizeof(int64_t), st));
-  k_regroup_plan<<<1, LT, 0, st>>>(C, G, np, scratch, scratch + cells, key_off);
+  note_launch(), k_regroup_plan<<<1, LT, 0, st>>>(C, G, np, scratch, scratch + cells, key_off);
   PHB_CUDA_TRY(cudaGetLastError());
   if (np > 0) {
     int64_t warps = np;
     int grid = (int)std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)num_sms() * 16);
-    k_regroup_copy<<<grid, 256, 0, st>>>(lo_in, aux_in, C, G, np, scratch, scratch + cells,
+    note_launch(), k_regroup_copy<<<grid, 256, 0, st>>>(lo_in, aux_in, C, G, np, scratch, scratch + cells,
                                          lo_out, aux_out);
     PHB_CUDA_TRY(cudaGetLastError());
   }

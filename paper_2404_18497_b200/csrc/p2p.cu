@@ -69,17 +69,17 @@ int launch_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_
   if (G < 1 || G > 64 || nparts < 1) return 1003;
   PeerTable t;
   for (int g = 0; g < G; ++g) t.lo[g] = lo_dst[g], t.bid[g] = bid_dst[g];
-  k_cursor_from_i64<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+  note_launch(), k_cursor_from_i64<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
       part_base, nparts, cursor);
   PHB_CUDA_TRY(cudaGetLastError());
   if (n <= 0) return 0;
   int64_t need = (n + 255) / 256;
   int grid = (int)std::min<int64_t>(need, (int64_t)num_sms() * 16);
   if (keys64)
-    k_scatter_p2p<<<grid, 256, 0, st>>>(U64KeysP{keys64}, n, seed, (uint64_t)nparts, entries,
+    note_launch(), k_scatter_p2p<<<grid, 256, 0, st>>>(U64KeysP{keys64}, n, seed, (uint64_t)nparts, entries,
                                         bcount, owner, cursor, t);
   else
-    k_scatter_p2p<<<grid, 256, 0, st>>>(ByteKeysP{buf, offsets}, n, seed, (uint64_t)nparts,
+    note_launch(), k_scatter_p2p<<<grid, 256, 0, st>>>(ByteKeysP{buf, offsets}, n, seed, (uint64_t)nparts,
                                         entries, bcount, owner, cursor, t);
   return (int)cudaGetLastError();
 }

@@ -6,6 +6,15 @@
 
 namespace phb {
 
+// Process-wide count of kernel launches issued by this library (every
+// <<<>>> site is written `note_launch(), kernel<<<...>>>(...)`); exported as
+// phb_launch_count() so bench.py reports launches it counted, not a constant.
+extern unsigned long long g_launch_count;
+inline int note_launch() {
+  __atomic_fetch_add(&g_launch_count, 1ull, __ATOMIC_RELAXED);
+  return 0;
+}
+
 int num_sms();
 
 int launch_murmur(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,

@@ -291,13 +291,13 @@ int launch_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* key
   if (nq <= 0) return 0;
   const int g = qgrid(nq);
   if (his)
-    k_query<2><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
+    note_launch(), k_query<2><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
                                   key_off, entries, bcount, seeds, s_sj, s_sb, out);
   else if (keys64)
-    k_query<0><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
+    note_launch(), k_query<0><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
                                   key_off, entries, bcount, seeds, s_sj, s_sb, out);
   else
-    k_query<1><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
+    note_launch(), k_query<1><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
                                   key_off, entries, bcount, seeds, s_sj, s_sb, out);
   return (int)cudaGetLastError();
 }
@@ -311,10 +311,10 @@ int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint6
   const int g = qgrid(nq);
   const ECol* c = reinterpret_cast<const ECol*>(cols);
   if (keys64)
-    k_query_enc<0><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
+    note_launch(), k_query_enc<0><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
                                       entries, bcount, section, c, mono, dsel, dstride, out);
   else
-    k_query_enc<1><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
+    note_launch(), k_query_enc<1><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
                                       entries, bcount, section, c, mono, dsel, dstride, out);
   return (int)cudaGetLastError();
 }
@@ -322,7 +322,7 @@ int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint6
 int launch_select_index(const uint8_t* section, const int64_t* cols, int64_t ncols,
                         int64_t stride, uint32_t* dsel, cudaStream_t st) {
   if (ncols <= 0) return 0;
-  k_select_index<<<(unsigned)ncols, 256, 0, st>>>(section, reinterpret_cast<const ECol*>(cols),
+  note_launch(), k_select_index<<<(unsigned)ncols, 256, 0, st>>>(section, reinterpret_cast<const ECol*>(cols),
                                                   stride, dsel);
   return (int)cudaGetLastError();
 }
@@ -330,7 +330,7 @@ int launch_select_index(const uint8_t* section, const int64_t* cols, int64_t nco
 int launch_verify(const int64_t* out, int64_t nq, int64_t n, uint32_t* bitmap, uint32_t* bad,
                   cudaStream_t st) {
   if (nq <= 0) return 0;
-  k_verify<<<qgrid(nq), 256, 0, st>>>(out, nq, n, bitmap, bad);
+  note_launch(), k_verify<<<qgrid(nq), 256, 0, st>>>(out, nq, n, bitmap, bad);
   return (int)cudaGetLastError();
 }
 

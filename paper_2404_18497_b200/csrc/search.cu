@@ -284,6 +284,7 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
     const uint64_t g = seed_hash(s);
     bool coll = false;
     uint32_t cmask = 0;  // per-round collision flags (s = 0 duplicate check)
+    __syncwarp();  // the previous candidate's find_d reads of pos16 precede this seed's writes
     if (k <= 32) {
       p0 = position(key0, g, m);
       const uint32_t peers = __match_any_sync(FULL, p0) & amask;
@@ -656,11 +657,13 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
         res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, 0, k > kg1 ? (1 << 30) : 1,
                               lane);
         if (res.status < 0) {
+          // batched instantiations hold 32 / G lanes per seed: only k <= 16
           if (k <= 8)
             res = small_bucket<4>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
-          else
+          else if (k <= kg1)
             res = small_bucket<2>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
-          if (res.status < 0)  // near the seed cap
+          // near the seed cap, or k > 16: single-seed steps until decided
+          while (res.status < 0)
             res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
                                   lane);
         }
@@ -731,7 +734,7 @@ int launch_search(const SearchArgs& a, cudaStream_t st) {
   int64_t cap = (int64_t)num_sms() * per_sm;
   int grid = (int)(want < cap ? want : cap);
   PHB_CUDA_TRY(cudaMemsetAsync(a.queue, 0, sizeof(uint32_t), st));
-  k_search<<<grid, WARPS * 32, per_cta, st>>>(a, plan);
+  note_launch(), k_search<<<grid, WARPS * 32, per_cta, st>>>(a, plan);
   return (int)cudaGetLastError();
 }
 

@@ -66,6 +66,13 @@ class DeviceOps:
         self.table = tabulate(self.spec)
         self.entries = device_table(self.table, self.dev)
         self.B = config.bucket_count
+        self.peer: PeerBuffers | None = None  # p2p receive buffers, kept across builds
+
+    def close(self) -> None:
+        """Collective: unmap the peers' receive buffers and free our own."""
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
 
     def stage(self, keys) -> DeviceKeys:
         return to_device(keys, self.dev)
@@ -234,11 +241,18 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
         total_counts = C.sum(0).to(torch.int32)
         key_off_g, deltas, stats = ops.layout(total_counts, n, nparts)
         C_owned = C[:, p_lo:p_hi]
-        m_max = int(C_owned.sum(0).max().item()) if np_g else 0
+        # one small host read: every rank's receive count and the owned max size
+        bt = torch.tensor(bounds, device=C.device)
+        csum = torch.zeros(nparts + 1, dtype=torch.int64, device=C.device)
+        torch.cumsum(total_counts.to(torch.int64), 0, out=csum[1:])
+        own_max = (total_counts[p_lo:p_hi].max().to(torch.int64).reshape(1) if np_g
+                   else torch.zeros(1, dtype=torch.int64, device=C.device))
+        small = torch.cat([csum[bt[1:]] - csum[bt[:-1]], own_max]).cpu().tolist()
+        recv_all, m_max = small[:world], int(small[world])
         routed = None
         if transport == "p2p":
             # 3-5 fused: records land partition-grouped in the owner's buffer
-            routed = _route_p2p(ops, dk, seed, nparts, C, bounds, rank, world, group)
+            routed = _route_p2p(ops, dk, seed, nparts, C, bounds, rank, world, group, recv_all)
             if routed is None:  # peer mapping unavailable on some rank: collective fallback
                 transport = "nccl"
         if routed is not None:
@@ -273,8 +287,6 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
         else:
             seeds_own = torch.zeros((config.bucket_count, 0), dtype=torch.int64, device=C.device)
             bad, code, trials = nparts, 0, 0
-        if route is not None:  # every rank, even one without partitions (barrier inside)
-            route.release_after_search()
         flag = torch.tensor([bad, trials], dtype=torch.int64, device=C.device)
         red = flag.clone()
         dist.all_reduce(red[0:1], op=dist.ReduceOp.MIN, group=group)
@@ -322,21 +334,94 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
         "input most likely contains duplicate keys")
 
 
-class _Route:
-    """CUDA-IPC peer buffers of one p2p routing step."""
+class PeerBuffers:
+    """CUDA-IPC receive buffers of the fused p2p route, allocated once per
+    DeviceOps and kept mapped in every peer across builds; they grow
+    (collectively) only when some rank must receive more records than its
+    buffer holds. Every rank derives every rank's receive count from the
+    all-gathered per-partition counts, so the grow decision needs no extra
+    collective."""
 
-    def __init__(self, lo_ptr, bid_ptr, n, peers, group):
-        self.lo_ptr, self.bid_ptr, self.n, self.peers, self.group = lo_ptr, bid_ptr, n, peers, group
+    def __init__(self, group, rank: int, world: int):
+        self.group, self.rank, self.world = group, rank, world
+        self.caps = [0] * world          # records per rank (identical on every rank)
+        self.lo_p = ctypes.c_void_p()    # own receive buffers
+        self.bid_p = ctypes.c_void_p()
+        self.lo_ptrs = (ctypes.c_void_p * world)()
+        self.bid_ptrs = (ctypes.c_void_p * world)()
+        self.opened: list[int] = []      # mapped peer buffers (not ours)
+        self.maps = 0                    # how many times the buffers were (re)mapped
 
-    def release_after_search(self):
+    def _unmap(self) -> None:
         L = _native.lib()
         _native.check(L.phb_sync(_native.stream()), "phb_sync")
-        for p in self.peers:  # mapped peer buffers (not ours)
-            _native.check(L.phb_ipc_close(p), "phb_ipc_close")
-        dist.barrier(group=self.group)  # every peer unmapped our buffer
-        _native.check(L.phb_ipc_free(self.lo_ptr), "phb_ipc_free")
-        _native.check(L.phb_ipc_free(self.bid_ptr), "phb_ipc_free")
-        self.peers = []
+        for ptr in self.opened:
+            L.phb_ipc_close(ptr)
+        self.opened = []
+        dist.barrier(group=self.group)  # every peer unmapped our buffers
+        if self.lo_p.value:
+            L.phb_ipc_free(self.lo_p)
+            L.phb_ipc_free(self.bid_p)
+        self.lo_p, self.bid_p = ctypes.c_void_p(), ctypes.c_void_p()
+
+    def close(self) -> None:
+        self._unmap()
+        self.caps = [0] * self.world
+
+    def ensure(self, recv: list[int], comm_dev) -> bool:
+        """Make every rank's buffer hold recv[g] records (collective when
+        any rank grows). False if some rank cannot map a peer buffer."""
+        if all(r <= c for r, c in zip(recv, self.caps)) and self.lo_p.value:
+            return True
+        L = _native.lib()
+        self._unmap()
+        # 2% headroom so that the next builds (retries, other seeds) fit
+        self.caps = [max(c, int(r * 1.02) + 4096) for r, c in zip(recv, self.caps)]
+        cap = self.caps[self.rank]
+        _native.check(L.phb_ipc_alloc(cap * 8, ctypes.byref(self.lo_p)), "phb_ipc_alloc")
+        _native.check(L.phb_ipc_alloc(cap * 2, ctypes.byref(self.bid_p)), "phb_ipc_alloc")
+        hbuf = np.zeros(128, np.uint8)
+        _native.check(L.phb_ipc_handle(self.lo_p, hbuf.ctypes.data_as(ctypes.c_void_p)),
+                      "phb_ipc_handle")
+        _native.check(L.phb_ipc_handle(self.bid_p, hbuf[64:].ctypes.data_as(ctypes.c_void_p)),
+                      "phb_ipc_handle")
+        mine = torch.from_numpy(hbuf).to(comm_dev)
+        allh = [torch.empty_like(mine) for _ in range(self.world)]
+        dist.all_gather(allh, mine, group=self.group)
+        ok = True
+        for g in range(self.world):
+            if g == self.rank:
+                self.lo_ptrs[g], self.bid_ptrs[g] = self.lo_p.value, self.bid_p.value
+                continue
+            h = np.ascontiguousarray(allh[g].cpu().numpy())
+            a, b = ctypes.c_void_p(), ctypes.c_void_p()
+            if L.phb_ipc_open(h.ctypes.data_as(ctypes.c_void_p), ctypes.byref(a)) != 0:
+                ok = False
+                break
+            self.opened.append(a.value)
+            if L.phb_ipc_open(h[64:].ctypes.data_as(ctypes.c_void_p), ctypes.byref(b)) != 0:
+                ok = False
+                break
+            self.opened.append(b.value)
+            self.lo_ptrs[g], self.bid_ptrs[g] = a.value, b.value
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=comm_dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        self.maps += 1
+        if int(flag.item()) == 0:
+            self.close()
+            return False
+        return True
+
+
+def _fence(group, dev) -> None:
+    """Order every rank's peer stores before the owners' reads. NCCL: a
+    1-element all_reduce enqueued on the stream (device-side ordering, no
+    host sync); other backends: stream sync + barrier."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(torch.zeros(1, dtype=torch.int32, device=dev), group=group)
+    else:
+        _native.check(_native.lib().phb_sync(_native.stream()), "phb_sync")
+        dist.barrier(group=group)
 
 
 class _PtrTensor:
@@ -353,10 +438,19 @@ class _PtrTensor:
 
 
 def _route_p2p(ops: DeviceOps, dk: DeviceKeys, seed: int, nparts: int, C: torch.Tensor,
-               bounds: list[int], rank: int, world: int, group):
-    """Fused K3 + all-to-all over peer memory (phb_scatter_p2p)."""
+               bounds: list[int], rank: int, world: int, group, recv_all: list[int]):
+    """Fused K3 + all-to-all over peer memory (phb_scatter_p2p) into the
+    persistent receive buffers. The next build's first collective (the
+    count all_gather, stream-ordered after this rank's search) orders the
+    owners' reads before the sources' next stores."""
     L = _native.lib()
     dev = ops.dev
+    if ops.peer is None:
+        ops.peer = PeerBuffers(group, rank, world)
+    if not ops.peer.ensure(recv_all, C.device):
+        ops.peer = None
+        return None
+    pb = ops.peer
     total = C.sum(0)                                       # [nparts] global counts
     ex = torch.zeros(nparts + 1, dtype=torch.int64, device=dev)
     torch.cumsum(total.to(dev), 0, out=ex[1:])
@@ -368,59 +462,18 @@ def _route_p2p(ops: DeviceOps, dk: DeviceKeys, seed: int, nparts: int, C: torch.
     before = (C[:rank].sum(0) if rank else torch.zeros_like(total)).to(dev)
     part_base = (ex[:-1] - start + before).contiguous()   # my first slot per partition
     p_lo, p_hi = bounds[rank], bounds[rank + 1]
-    recv_n = int((ex[p_hi] - ex[p_lo]).item())
-    # my receive buffers (IPC-able cudaMalloc) and the peers' handles
-    lo_p, bid_p = ctypes.c_void_p(), ctypes.c_void_p()
-    _native.check(L.phb_ipc_alloc(max(recv_n, 1) * 8, ctypes.byref(lo_p)), "phb_ipc_alloc")
-    _native.check(L.phb_ipc_alloc(max(recv_n, 1) * 2, ctypes.byref(bid_p)), "phb_ipc_alloc")
-    hbuf = np.zeros(128, np.uint8)
-    _native.check(L.phb_ipc_handle(lo_p, hbuf.ctypes.data_as(ctypes.c_void_p)), "phb_ipc_handle")
-    _native.check(L.phb_ipc_handle(bid_p, hbuf[64:].ctypes.data_as(ctypes.c_void_p)),
-                  "phb_ipc_handle")
-    comm_dev = C.device
-    mine = torch.from_numpy(hbuf).to(comm_dev)
-    allh = [torch.empty_like(mine) for _ in range(world)]
-    dist.all_gather(allh, mine, group=group)
-    lo_ptrs = (ctypes.c_void_p * world)()
-    bid_ptrs = (ctypes.c_void_p * world)()
-    opened = []
-    ok = True
-    for g in range(world):
-        if g == rank:
-            lo_ptrs[g], bid_ptrs[g] = lo_p.value, bid_p.value
-            continue
-        h = np.ascontiguousarray(allh[g].cpu().numpy())
-        a, b = ctypes.c_void_p(), ctypes.c_void_p()
-        if L.phb_ipc_open(h.ctypes.data_as(ctypes.c_void_p), ctypes.byref(a)) != 0:
-            ok = False
-            break
-        opened.append(a.value)
-        if L.phb_ipc_open(h[64:].ctypes.data_as(ctypes.c_void_p), ctypes.byref(b)) != 0:
-            ok = False
-            break
-        opened.append(b.value)
-        lo_ptrs[g], bid_ptrs[g] = a.value, b.value
-    flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=comm_dev)
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
-    if int(flag.item()) == 0:  # undo and let every rank take the NCCL route
-        for ptr in opened:
-            L.phb_ipc_close(ptr)
-        dist.barrier(group=group)
-        L.phb_ipc_free(lo_p)
-        L.phb_ipc_free(bid_p)
-        return None
+    recv_n = recv_all[rank]
     cursor = torch.empty(nparts, dtype=torch.int32, device=dev)
     P = _native.ptr
     _native.check(L.phb_scatter_p2p(
         None if dk.is_u64 else P(dk.buf), None if dk.is_u64 else P(dk.offsets),
         P(dk.keys64) if dk.is_u64 else None, dk.n, seed, nparts, P(ops.entries), ops.B,
-        P(part_base), P(owner), lo_ptrs, bid_ptrs, world, P(cursor), _native.stream()),
+        P(part_base), P(owner), pb.lo_ptrs, pb.bid_ptrs, world, P(cursor), _native.stream()),
         "phb_scatter_p2p")
-    _native.check(L.phb_sync(_native.stream()), "phb_sync")
-    dist.barrier(group=group)  # every source finished writing into every owner
+    _fence(group, dev)  # every source finished writing into every owner
     key_off_own = (ex[p_lo:p_hi + 1] - ex[p_lo]).contiguous()
-    route = _Route(lo_p.value, bid_p.value, recv_n, opened, group)
-    return (_PtrTensor(lo_p.value, recv_n), _PtrTensor(bid_p.value, recv_n), key_off_own, route)
+    return (_PtrTensor(pb.lo_p.value, recv_n), _PtrTensor(pb.bid_p.value, recv_n), key_off_own,
+            None)
 
 
 class _EngineView:
