@@ -219,6 +219,26 @@ int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64
  * samples byte, nsamples}, byte offsets relative to section. Interleaved:
  * num_enc == bcount, encoder b-1 indexed by partition; mono: one encoder
  * indexed j*bcount + b-1. */
+/* Batched query over compact tables (seeds32 = phb_seed_table32 of the
+ * column-major [B][nparts] u64 matrix; part2 = phb_part_table32 of key_off,
+ * requires n < 2^32): same outputs as phb_query with half the gather
+ * footprint, one 8-byte partition gather and no division, four u64 keys
+ * per thread. key_off (int64 [nparts + 1], may be NULL): large u64 batches
+ * whose u32 offsets fit in shared memory (~49k partitions) read them there
+ * and make a single random gather per query. u64 keys and out must be 16-byte aligned (PHB_E_ARGS
+ * otherwise; use phb_query). Replaces query_many_kernel (_kernels.py:379-397). */
+int phb_query32(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t nq,
+                uint64_t seed, int64_t n, int64_t nparts, const int64_t* key_off,
+                const uint32_t* part2, const double* entries, int32_t bcount,
+                const uint32_t* seeds32, int64_t* out, void* stream);
+/* key_off (int64 [nparts + 1]) -> part2 (u32 (offset, end) pairs [nparts]). */
+int phb_part_table32(const int64_t* key_off, int64_t nparts, uint32_t* part2, void* stream);
+/* u64 seeds [B][nparts] -> u32 (s << 16) | d with p = s m + d (m from
+ * key_off); *overflow (device u32, zeroed by the caller) becomes 1 if some
+ * entry does not fit (s >= 2^16 or m > 2^16). */
+int phb_seed_table32(const uint64_t* seeds, const int64_t* key_off, int64_t nparts, int64_t count,
+                     uint32_t* out, uint32_t* overflow, void* stream);
+
 int phb_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                       int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                       const int64_t* key_off, const double* entries, int32_t bcount,

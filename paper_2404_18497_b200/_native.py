@@ -45,6 +45,9 @@ SIGNATURES = {
     "phb_encode_shard_plan": [P, I64, I64, I64, I32, I32, I32, P, P, P, P, P, P],
     "phb_encode_shard_write": [P, I64, I64, I64, I32, I32, I32, P, P, P, I32, P, P, SZ, P],
     "phb_query": [P, P, P, I64, U64, I64, I64, P, P, I32, P, I64, I64, P, P],
+    "phb_query32": [P, P, P, I64, U64, I64, I64, P, P, P, I32, P, P, P],
+    "phb_seed_table32": [P, P, I64, I64, P, P, P],
+    "phb_part_table32": [P, I64, P, P],
     "phb_query_encoded": [P, P, P, I64, U64, I64, I64, P, P, I32, P, P, I32, I32, P, I64, P, P],
     "phb_select_index": [P, P, I64, I64, P, P],
     "phb_verify": [P, I64, I64, P, P, P],

@@ -410,6 +410,29 @@ int phb_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64
                       entries, (uint32_t)bcount, seeds, s_sj, s_sb, out, S(stream));
 }
 
+int phb_query32(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t nq,
+                uint64_t seed, int64_t n, int64_t nparts, const int64_t* key_off,
+                const uint32_t* part2, const double* entries, int32_t bcount,
+                const uint32_t* seeds32, int64_t* out, void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (nparts < 1 || !seeds32 || !part2 || n >= (int64_t)1 << 32) return PHB_E_ARGS;
+  return launch_query32(buf, offsets, keys64, nq, seed, n, nparts, key_off,
+                        reinterpret_cast<const uint2*>(part2), entries, (uint32_t)bcount, seeds32,
+                        out, S(stream));
+}
+
+int phb_part_table32(const int64_t* key_off, int64_t nparts, uint32_t* part2, void* stream) {
+  if (nparts < 0 || (nparts > 0 && (!key_off || !part2))) return PHB_E_ARGS;
+  return launch_part_table32(key_off, nparts, reinterpret_cast<uint2*>(part2), S(stream));
+}
+
+int phb_seed_table32(const uint64_t* seeds, const int64_t* key_off, int64_t nparts, int64_t count,
+                     uint32_t* out, uint32_t* overflow, void* stream) {
+  if (count < 0 || nparts < 1 || (count > 0 && (!seeds || !key_off || !out || !overflow)))
+    return PHB_E_ARGS;
+  return launch_seed_table32(seeds, key_off, nparts, count, out, overflow, S(stream));
+}
+
 int phb_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                       int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                       const int64_t* key_off, const double* entries, int32_t bcount,

@@ -165,24 +165,98 @@ __device__ __forceinline__ Hash128 murmur3_bytes(const uint8_t* __restrict__ key
 // gamma = e[2048] if k >= 2048 else e[k] + (t - k) * (e[k+1] - e[k]);
 // b = clamp(ceil(gamma * B), 1, B). Each operation rounds on its own:
 // the explicit _rn intrinsics forbid FMA contraction.
-__device__ __forceinline__ uint32_t bucket_of(const double* __restrict__ e, uint64_t hi,
-                                              uint32_t bcount) {
-  uint64_t xb = mix64(hi ^ BUCKET_SALT);
-  double x = __dmul_rn(__dadd_rn(__ull2double_rn(xb), 1.0), 0x1p-64);
-  double t = __dmul_rn(x, 2048.0);
-  int k = __double2int_rz(t);
-  double g;
-  if (k >= GRID) {
-    g = __ldg(e + GRID);
-  } else {
-    double ek = __ldg(e + k), ek1 = __ldg(e + k + 1);
-    g = __dadd_rn(ek, __dmul_rn(__dsub_rn(t, (double)k), __dsub_rn(ek1, ek)));
-  }
+//
+// Default: the direct conversions (I2F / F2I / FRND on the XU pipe).
+// PHB_BUCKET_FP64 builds an XU-free form, bit-identical (edge cases in
+// tools/bucket_edge.py): an integer below 2^32 becomes a double as
+// (2^52 + v) - 2^52 on the FP64 pipe, a u64 is rounded once by an FMA of its
+// two exact halves, int(t) and ceil(y) come from the 2^52
+// round-to-integer trick with a one-step correction. Measured slower in
+// the query (1.42 vs 1.14 ms at C2: a longer dependent chain; the XU pipe
+// was at 10%, not the limit) and neutral in the scatter, so it is off.
+__device__ __forceinline__ double f64_of_u32(uint32_t v) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)v), 0x1p52);
+}
+__device__ __forceinline__ double f64_rn_of_u64(uint64_t v) {  // == __ull2double_rn(v)
+  return __fma_rn(f64_of_u32((uint32_t)(v >> 32)), 0x1p32, f64_of_u32((uint32_t)v));
+}
+
+struct BucketT {
+  double t, kd;  // t = 2048 x and (double)k
+  int k;         // k = int(t), t in [0, 2048]
+};
+#ifndef PHB_BUCKET_FP64
+__device__ __forceinline__ BucketT bucket_t(uint64_t hi) {
+  const uint64_t xb = mix64(hi ^ BUCKET_SALT);
+  const double x = __dmul_rn(__dadd_rn(__ull2double_rn(xb), 1.0), 0x1p-64);
+  const double t = __dmul_rn(x, 2048.0);
+  const int k = __double2int_rz(t);
+  return {t, (double)k, k};
+}
+__device__ __forceinline__ uint32_t bucket_finish(double g, uint32_t bcount) {
   double y = __dmul_rn(g, (double)bcount);
   double c = ceil(y);
   if (c < 1.0) return 1u;
   if (c > (double)bcount) return bcount;
   return (uint32_t)c;
+}
+#else
+__device__ __forceinline__ BucketT bucket_t(uint64_t hi) {
+  const uint64_t xb = mix64(hi ^ BUCKET_SALT);
+  const double x = __dmul_rn(__dadd_rn(f64_rn_of_u64(xb), 1.0), 0x1p-64);
+  const double t = __dmul_rn(x, 2048.0);
+  const double r = __dadd_rn(t, 0x1p52);  // 2^52 + round-to-nearest-even(t)
+  double kd = __dsub_rn(r, 0x1p52);
+  int k = __double2loint(r);
+  if (kd > t) {  // rounded up: truncate
+    kd = __dsub_rn(kd, 1.0);
+    k -= 1;
+  }
+  return {t, kd, k};
+}
+__device__ __forceinline__ uint32_t bucket_finish(double g, uint32_t bcount) {
+  const double y = __dmul_rn(g, f64_of_u32(bcount));  // y in [0, B]
+  const double r = __dadd_rn(y, 0x1p52);
+  uint32_t c = (uint32_t)__double2loint(r);  // round-to-nearest-even(y)
+  if (__dsub_rn(r, 0x1p52) < y) c += 1;      // ceil
+  if (c < 1u) return 1u;
+  if (c > bcount) return bcount;
+  return c;
+}
+#endif
+
+__device__ __forceinline__ uint32_t bucket_of(const double* __restrict__ e, uint64_t hi,
+                                              uint32_t bcount) {
+  const BucketT b = bucket_t(hi);
+  double g;
+  if (b.k >= GRID) {
+    g = __ldg(e + GRID);
+  } else {
+    const double ek = __ldg(e + b.k), ek1 = __ldg(e + b.k + 1);
+    g = __dadd_rn(ek, __dmul_rn(__dsub_rn(b.t, b.kd), __dsub_rn(ek1, ek)));
+  }
+  return bucket_finish(g, bcount);
+}
+
+// bucket_of over a shared-memory copy of the table as adjacent pairs
+// tab[k] = (e[k], e[k+1]) for k < GRID and tab[GRID] = (e[GRID], e[GRID]):
+// one 16-byte shared load instead of two random L1 gathers per key.
+constexpr int BUCKET_TAB = GRID + 1;  // double2 entries (32 KB)
+
+__device__ __forceinline__ void load_bucket_pairs(const double* __restrict__ entries,
+                                                  double2* tab) {
+  for (int k = threadIdx.x; k <= GRID; k += blockDim.x)
+    tab[k] = make_double2(__ldg(entries + k), __ldg(entries + (k < GRID ? k + 1 : k)));
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t bucket_of_pairs(const double2* tab, uint64_t hi,
+                                                    uint32_t bcount) {
+  const BucketT b = bucket_t(hi);
+  const double2 e = tab[b.k < GRID ? b.k : GRID];
+  const double g = b.k >= GRID ? e.x : __dadd_rn(e.x, __dmul_rn(__dsub_rn(b.t, b.kd),
+                                                                  __dsub_rn(e.y, e.x)));
+  return bucket_finish(g, bcount);
 }
 
 __device__ __forceinline__ uint32_t position(uint64_t lo, uint64_t g, uint32_t m) {

@@ -86,11 +86,13 @@ __global__ void __launch_bounds__(256) k_scatter(K keys, int64_t n, uint64_t see
                                                  uint32_t bcount, uint32_t* __restrict__ cursor,
                                                  uint64_t* __restrict__ lo_out,
                                                  uint16_t* __restrict__ bid_out) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     Hash128 h = keys.hash(i, seed);
     uint32_t j = (uint32_t)mulhi(h.hi, nparts);
-    uint32_t b = bucket_of(entries, h.hi, bcount);
+    uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
     uint32_t pos = atomicAdd(cursor + j, 1u);
     lo_out[pos] = h.lo;
     bid_out[pos] = (uint16_t)b;
@@ -106,6 +108,8 @@ __global__ void __launch_bounds__(256) k_scatter_u64x4(const ulonglong2* __restr
                                                        uint32_t* __restrict__ cursor,
                                                        uint64_t* __restrict__ lo_out,
                                                        uint16_t* __restrict__ bid_out) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
   const int64_t nq = n >> 2;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
        q += (int64_t)gridDim.x * blockDim.x) {
@@ -117,13 +121,21 @@ __global__ void __launch_bounds__(256) k_scatter_u64x4(const ulonglong2* __restr
     for (int e = 0; e < 4; ++e) {
       const Hash128 h = murmur3_u64(k[e], seed);
       lo[e] = h.lo;
-      b[e] = bucket_of(entries, h.hi, bcount);
+      b[e] = bucket_of_pairs(tab, h.hi, bcount);
       pos[e] = atomicAdd(cursor + (uint32_t)mulhi(h.hi, nparts), 1u);
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
+#if defined(PHB_K3_REC16)  // measurement variant: one 16-byte record store per key
+      reinterpret_cast<ulonglong2*>(lo_out)[pos[e]] = make_ulonglong2(lo[e], b[e]);
+#else
+#ifndef PHB_K3_NOLO  // measurement variants (invalid output): which store costs
       lo_out[pos[e]] = lo[e];
+#endif
+#ifndef PHB_K3_NOBID
       bid_out[pos[e]] = (uint16_t)b[e];
+#endif
+#endif
     }
   }
   // tail (n % 4 keys)
@@ -133,7 +145,7 @@ __global__ void __launch_bounds__(256) k_scatter_u64x4(const ulonglong2* __restr
     const Hash128 h = murmur3_u64(__ldg(keys + t), seed);
     const uint32_t pos = atomicAdd(cursor + (uint32_t)mulhi(h.hi, nparts), 1u);
     lo_out[pos] = h.lo;
-    bid_out[pos] = (uint16_t)bucket_of(entries, h.hi, bcount);
+    bid_out[pos] = (uint16_t)bucket_of_pairs(tab, h.hi, bcount);
   }
 }
 
@@ -155,6 +167,8 @@ __global__ void __launch_bounds__(256) k_scatter_padded_u64x4(
     const double* __restrict__ entries, uint32_t bcount, uint32_t cap,
     uint32_t* __restrict__ cursor, uint64_t* __restrict__ lo_out, uint16_t* __restrict__ bid_out,
     uint32_t* __restrict__ overflow) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
   const int64_t nq = n >> 2;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
        q += (int64_t)gridDim.x * blockDim.x) {
@@ -167,7 +181,7 @@ __global__ void __launch_bounds__(256) k_scatter_padded_u64x4(
       const Hash128 h = murmur3_u64(k[e], seed);
       const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
       lo[e] = h.lo;
-      b[e] = bucket_of(entries, h.hi, bcount);
+      b[e] = bucket_of_pairs(tab, h.hi, bcount);
       lim[e] = (j + 1) * cap;
       pos[e] = atomicAdd(cursor + j, 1u);
     }
@@ -189,7 +203,7 @@ __global__ void __launch_bounds__(256) k_scatter_padded_u64x4(
     const uint32_t pos = atomicAdd(cursor + j, 1u);
     if (pos < (j + 1) * cap) {
       lo_out[pos] = h.lo;
-      bid_out[pos] = (uint16_t)bucket_of(entries, h.hi, bcount);
+      bid_out[pos] = (uint16_t)bucket_of_pairs(tab, h.hi, bcount);
     } else {
       atomicOr(overflow, 1u);
     }
@@ -248,9 +262,11 @@ __global__ void __launch_bounds__(1024, 1) k_hash_count_u64x4(const ulonglong2* 
 __global__ void __launch_bounds__(256) k_bucket_ids(const uint64_t* __restrict__ his, int64_t n,
                                                     const double* __restrict__ entries,
                                                     uint32_t bcount, uint16_t* __restrict__ bid) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    bid[i] = (uint16_t)bucket_of(entries, __ldg(his + i), bcount);
+    bid[i] = (uint16_t)bucket_of_pairs(tab, __ldg(his + i), bcount);
 }
 
 static inline int grid_for(int64_t n, int per_sm = 16) {
@@ -284,8 +300,11 @@ int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t
   int g = grid_for(n);
   if (keys64 && aligned16(keys64) && nparts > SMEM_HIST_MAX && nparts <= SMEM_HIST_MAX_BIG) {
     size_t sh = nparts * sizeof(uint32_t);
+    // the largest histogram this path takes (not this launch's size): a
+    // concurrent launch from another host thread must not see a lower cap
     PHB_CUDA_TRY(cudaFuncSetAttribute(k_hash_count_u64x4,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(SMEM_HIST_MAX_BIG * sizeof(uint32_t))));
     int64_t need = ((n >> 2) + 1023) / 1024;
     int gb = (int)std::max<int64_t>(1, std::min<int64_t>(need, num_sms()));
     note_launch(), k_hash_count_u64x4<<<gb, 1024, sh, st>>>(reinterpret_cast<const ulonglong2*>(keys64), n,

@@ -27,11 +27,13 @@ __global__ void __launch_bounds__(256)
     k_scatter_p2p(K keys, int64_t n, uint64_t seed, uint64_t nparts,
                   const double* __restrict__ entries, uint32_t bcount,
                   const uint8_t* __restrict__ owner, uint32_t* __restrict__ cursor, PeerTable peers) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const Hash128 h = keys.hash(i, seed);
     const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
-    const uint32_t b = bucket_of(entries, h.hi, bcount);
+    const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
     const uint32_t g = __ldg(owner + j);
     const uint32_t pos = atomicAdd(cursor + j, 1u);
     peers.lo[g][pos] = h.lo;

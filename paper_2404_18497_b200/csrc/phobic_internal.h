@@ -84,6 +84,14 @@ int launch_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* key
                  int64_t nparts, const int64_t* key_off, const double* entries, uint32_t bcount,
                  const uint64_t* seeds, int64_t s_sj, int64_t s_sb, int64_t* out,
                  cudaStream_t st);
+int launch_query32(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t nq,
+                   uint64_t seed, int64_t n, int64_t nparts, const int64_t* key_off,
+                   const uint2* part2,
+                   const double* entries, uint32_t bcount, const uint32_t* seeds32, int64_t* out,
+                   cudaStream_t st);
+int launch_part_table32(const int64_t* key_off, int64_t nparts, uint2* part2, cudaStream_t st);
+int launch_seed_table32(const uint64_t* seeds, const int64_t* key_off, int64_t nparts,
+                        int64_t count, uint32_t* out, uint32_t* overflow, cudaStream_t st);
 int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                          int64_t nq, uint64_t seed, int64_t n, int64_t nparts,
                          const int64_t* key_off, const double* entries, uint32_t bcount,

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256)
        i += (int64_t)gridDim.x * blockDim.x) {
     Hash128 h;
     if (MODE == 0) {
-      h = murmur3_u64(__ldg(keys64 + i), seed);
+      h = murmur3_u64(__ldcs(keys64 + i), seed);  // streaming: keep the tables in L2
     } else if (MODE == 1) {
       int64_t a = __ldg(offsets + i), b = __ldg(offsets + i + 1);
       h = murmur3_bytes(buf + a, b - a, seed);
@@ -55,7 +55,177 @@ __global__ void __launch_bounds__(256)
       if (pos >= mu) pos -= mu;
       r = offj + (int64_t)pos;
     }
-    out[i] = r;
+    __stcs(out + i, r);
+  }
+}
+
+// ---- K7q: the same query over compact tables, for structures where every
+// seed and every key offset fits 32 bits (far beyond the BASELINE sizes:
+// the largest C3 seed is ~2^24, n < 2^32):
+//   * seeds32 [B][nparts] u32 = (s << 16) | d for p = s m + d: half the
+//     gather footprint of the u64 matrix (44 MB at C2, L2-resident) and no
+//     division per query (needs s < 2^16; the C2 maximum is ~3,500);
+//   * part2 [nparts] (offset, end) u32 pairs: one 8-byte gather per query
+//     instead of two 8-byte key_off loads;
+//   * the bucket table as (e[k], e[k+1]) pairs in shared memory: one
+//     16-byte shared load instead of two random L1 gathers per query (those
+//     queued behind the global loads: lg_throttle in the profile);
+//   * u64 keys: four per thread, so four independent gather chains overlap.
+__device__ __forceinline__ int64_t finish_query(uint64_t lo, uint2 pe, int64_t n, uint32_t sd) {
+  const int64_t offj = pe.x;
+  if (pe.y <= pe.x) return offj < n ? offj : n - 1;
+  const uint32_t mu = pe.y - pe.x;
+  const uint32_t sq = sd >> 16, d = sd & 0xffffu;  // p = sq * m + d, split once at table build
+  const uint64_t g = mix64((uint64_t)sq ^ POSITION_SALT);
+  uint32_t pos = (uint32_t)mulhi(mix64(lo ^ g), (uint64_t)mu) + d;  // (base + p) mod m
+  if (pos >= mu) pos -= mu;
+  return offj + (int64_t)pos;
+}
+
+__global__ void __launch_bounds__(256)
+    k_query32_u64x4(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
+                    uint64_t nparts, const uint2* __restrict__ part2,
+                    const double* __restrict__ entries, uint32_t bcount,
+                    const uint32_t* __restrict__ seeds32, longlong2* __restrict__ out2) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
+  const int64_t nv = nq >> 2;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    // streaming keys / outputs are marked evict-first so the tables stay in L2
+    const ulonglong2 ka = __ldcs(keys2 + 2 * v), kc = __ldcs(keys2 + 2 * v + 1);
+    const uint64_t k[4] = {ka.x, ka.y, kc.x, kc.y};
+    uint64_t hi[4], lo[4], j[4];
+    uint2 pe[4];
+    uint32_t p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const Hash128 h = murmur3_u64(k[e], seed);
+      hi[e] = h.hi;
+      lo[e] = h.lo;
+      j[e] = mulhi(h.hi, nparts);
+      pe[e] = __ldg(part2 + j[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t b = bucket_of_pairs(tab, hi[e], bcount);
+      p[e] = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + (int64_t)j[e]);
+    }
+    int64_t r[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r[e] = finish_query(lo[e], pe[e], n, p[e]);
+    __stcs(out2 + 2 * v, make_longlong2(r[0], r[1]));
+    __stcs(out2 + 2 * v + 1, make_longlong2(r[2], r[3]));
+  }
+  // tail (nq % 4 keys)
+  const int64_t t = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < nq) {
+    const Hash128 h = murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
+    const uint64_t jj = mulhi(h.hi, nparts);
+    const uint2 q = __ldg(part2 + jj);
+    const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
+    const uint32_t pp = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + (int64_t)jj);
+    reinterpret_cast<int64_t*>(out2)[t] = finish_query(h.lo, q, n, pp);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_query32_bytes(const uint8_t* __restrict__ buf, const int64_t* __restrict__ offsets,
+                    int64_t nq, uint64_t seed, int64_t n, uint64_t nparts,
+                    const uint2* __restrict__ part2, const double* __restrict__ entries,
+                    uint32_t bcount, const uint32_t* __restrict__ seeds32,
+                    int64_t* __restrict__ out) {
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = __ldg(offsets + i), e = __ldg(offsets + i + 1);
+    const Hash128 h = murmur3_bytes(buf + a, e - a, seed);
+    const uint64_t j = mulhi(h.hi, nparts);
+    const uint2 q = __ldg(part2 + j);
+    const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
+    const uint32_t p = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + (int64_t)j);
+    out[i] = finish_query(h.lo, q, n, p);
+  }
+}
+
+// K7s: K7q with the partition offsets in shared memory (u32 key_off[0..nparts],
+// 4 B per partition: up to ~49k partitions next to the 32 KB bucket table,
+// i.e. C2's 40k). A query then makes ONE random global gather (its seed),
+// not two: the random gathers are what the L1 tag stage serialises (32
+// distinct lines per warp instruction). One 1024-thread CTA per SM, the
+// tables loaded once per CTA.
+__global__ void __launch_bounds__(1024, 1)
+    k_query32s_u64x4(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
+                     uint64_t nparts, const int64_t* __restrict__ key_off,
+                     const double* __restrict__ entries, uint32_t bcount,
+                     const uint32_t* __restrict__ seeds32, longlong2* __restrict__ out2) {
+  extern __shared__ __align__(16) unsigned char q_smem[];
+  double2* const tab = reinterpret_cast<double2*>(q_smem);
+  uint32_t* const koff = reinterpret_cast<uint32_t*>(tab + BUCKET_TAB);
+  for (int64_t j = threadIdx.x; j <= (int64_t)nparts; j += blockDim.x)
+    koff[j] = (uint32_t)__ldg(key_off + j);
+  load_bucket_pairs(entries, tab);  // ends with __syncthreads
+  const int64_t nv = nq >> 2;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    // streaming keys / outputs are marked evict-first so the seed table stays in L2
+    const ulonglong2 ka = __ldcs(keys2 + 2 * v), kc = __ldcs(keys2 + 2 * v + 1);
+    const uint64_t k[4] = {ka.x, ka.y, kc.x, kc.y};
+    uint64_t lo[4];
+    uint2 pe[4];
+    uint32_t p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const Hash128 h = murmur3_u64(k[e], seed);
+      lo[e] = h.lo;
+      const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
+      const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
+      p[e] = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + j);
+      pe[e] = make_uint2(koff[j], koff[j + 1]);
+    }
+    int64_t r[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r[e] = finish_query(lo[e], pe[e], n, p[e]);
+    __stcs(out2 + 2 * v, make_longlong2(r[0], r[1]));
+    __stcs(out2 + 2 * v + 1, make_longlong2(r[2], r[3]));
+  }
+  const int64_t t = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < nq) {
+    const Hash128 h = murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
+    const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
+    const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
+    const uint32_t pp = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + j);
+    reinterpret_cast<int64_t*>(out2)[t] = finish_query(h.lo, make_uint2(koff[j], koff[j + 1]), n, pp);
+  }
+}
+
+// key_off (int64 [nparts + 1]) -> (offset, end) u32 pairs
+__global__ void k_part_table32(const int64_t* __restrict__ key_off, int64_t nparts,
+                               uint2* __restrict__ part2) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nparts;
+       j += (int64_t)gridDim.x * blockDim.x)
+    part2[j] = make_uint2((uint32_t)key_off[j], (uint32_t)key_off[j + 1]);
+}
+
+// u64 seed matrix [B][nparts] -> the (s << 16) | d table of K7q; *overflow
+// = 1 if some entry does not fit (s >= 2^16 or m > 2^16: the caller keeps
+// the u64 path then).
+__global__ void k_seed_table32(const uint64_t* __restrict__ seeds, const int64_t* __restrict__ key_off,
+                               int64_t nparts, int64_t count, uint32_t* __restrict__ out,
+                               uint32_t* __restrict__ overflow) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = i % nparts;
+    const int64_t m = key_off[j + 1] - key_off[j];
+    const uint64_t p = seeds[i];
+    uint32_t v = 0;
+    if (m > 0) {
+      const uint64_t sq = p / (uint64_t)m, d = p - sq * (uint64_t)m;
+      if (sq >= 65536u || m > 65536) atomicOr(overflow, 1u);
+      v = (uint32_t)((sq << 16) | d);
+    }
+    out[i] = v;
   }
 }
 
@@ -232,7 +402,7 @@ __global__ void __launch_bounds__(256)
        i += (int64_t)gridDim.x * blockDim.x) {
     Hash128 h;
     if (MODE == 0) {
-      h = murmur3_u64(__ldg(keys64 + i), seed);
+      h = murmur3_u64(__ldcs(keys64 + i), seed);  // streaming: keep the section in L2
     } else {
       int64_t a = __ldg(offsets + i), b = __ldg(offsets + i + 1);
       h = murmur3_bytes(buf + a, b - a, seed);
@@ -249,13 +419,13 @@ __global__ void __launch_bounds__(256)
           mono ? eget(sec, cols, (int64_t)j * bcount + (b - 1), dsel)
                : eget(sec, cols + (b - 1), (int64_t)j, dsel ? dsel + (int64_t)(b - 1) * dstride : nullptr);
       const uint64_t mu = (uint64_t)m;
-      const uint64_t s = p / mu;
+      const uint64_t s = (p >> 32) ? p / mu : (uint64_t)((uint32_t)p / (uint32_t)mu);
       const uint64_t d = p - s * mu;
       uint64_t pos = mulhi(mix64(h.lo ^ mix64(s ^ POSITION_SALT)), mu) + d;
       if (pos >= mu) pos -= mu;
       r = offj + (int64_t)pos;
     }
-    out[i] = r;
+    __stcs(out + i, r);
   }
 }
 
@@ -299,6 +469,54 @@ int launch_query(const uint8_t* buf, const int64_t* offsets, const uint64_t* key
   else
     note_launch(), k_query<1><<<g, 256, 0, st>>>(buf, offsets, keys64, his, los, nq, seed, n, (uint64_t)nparts,
                                   key_off, entries, bcount, seeds, s_sj, s_sb, out);
+  return (int)cudaGetLastError();
+}
+
+int launch_query32(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t nq,
+                   uint64_t seed, int64_t n, int64_t nparts, const int64_t* key_off,
+                   const uint2* part2,
+                   const double* entries, uint32_t bcount, const uint32_t* seeds32, int64_t* out,
+                   cudaStream_t st) {
+  if (nq <= 0) return 0;
+  if (keys64) {
+    if ((reinterpret_cast<uintptr_t>(keys64) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+      return 1003;  // PHB_E_ARGS: the 4-key vector path needs 16-byte alignment
+    const size_t sh = sizeof(double2) * BUCKET_TAB + sizeof(uint32_t) * (size_t)(nparts + 1);
+    int dev = 0, optin = 0;
+    PHB_CUDA_TRY(cudaGetDevice(&dev));
+    PHB_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (key_off && sh <= (size_t)optin && nq >= (int64_t)num_sms() * 4096) {
+      // the largest shared footprint this path takes (concurrent launches
+      // from other host threads must not see a lower cap)
+      PHB_CUDA_TRY(cudaFuncSetAttribute(k_query32s_u64x4,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      note_launch(), k_query32s_u64x4<<<num_sms(), 1024, sh, st>>>(
+          reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, key_off,
+          entries, bcount, seeds32, reinterpret_cast<longlong2*>(out));
+    } else {
+      note_launch(), k_query32_u64x4<<<qgrid((nq + 3) / 4), 256, 0, st>>>(
+          reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, part2,
+          entries, bcount, seeds32, reinterpret_cast<longlong2*>(out));
+    }
+  } else {
+    note_launch(), k_query32_bytes<<<qgrid(nq), 256, 0, st>>>(buf, offsets, nq, seed, n,
+                                                              (uint64_t)nparts, part2, entries,
+                                                              bcount, seeds32, out);
+  }
+  return (int)cudaGetLastError();
+}
+
+int launch_part_table32(const int64_t* key_off, int64_t nparts, uint2* part2, cudaStream_t st) {
+  if (nparts <= 0) return 0;
+  note_launch(), k_part_table32<<<qgrid(nparts), 256, 0, st>>>(key_off, nparts, part2);
+  return (int)cudaGetLastError();
+}
+
+int launch_seed_table32(const uint64_t* seeds, const int64_t* key_off, int64_t nparts,
+                        int64_t count, uint32_t* out, uint32_t* overflow, cudaStream_t st) {
+  if (count <= 0) return 0;
+  note_launch(), k_seed_table32<<<qgrid(count), 256, 0, st>>>(seeds, key_off, nparts, count, out,
+                                                              overflow);
   return (int)cudaGetLastError();
 }
 

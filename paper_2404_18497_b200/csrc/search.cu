@@ -763,8 +763,11 @@ int launch_search(const SearchArgs& a, cudaStream_t st) {
   int max_optin = 0;
   PHB_CUDA_TRY(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   if (per_cta > (size_t)max_optin) return 1002;  // PHB_E_PARTITION_TOO_LARGE
+  // the device's opt-in maximum, not this launch's size: host threads
+  // launching concurrently (compat_kernels under builder.py's thread pool)
+  // would otherwise race on the attribute and launch above each other's cap
   PHB_CUDA_TRY(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)per_cta));
+                                    max_optin));
   int per_sm = 0;
   PHB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, WARPS * 32,
                                                              per_cta));

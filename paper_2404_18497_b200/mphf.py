@@ -384,6 +384,29 @@ class Mphf:
     def num_partitions(self) -> int:
         return self._dev.nparts if self._layout is None else self._layout.num_partitions
 
+    def _query_tables32(self, seeds: torch.Tensor, key_off: torch.Tensor):
+        """The compact tables phb_query32 reads, built once per structure:
+        (s << 16) | d per seed (phb_seed_table32) and (offset, end) u32
+        partition pairs (phb_part_table32). None if an entry does not fit or
+        n >= 2^32 (phb_query on the u64 matrix then)."""
+        cached = getattr(self, "_tables32", None)
+        if cached is not None and cached[0] is seeds:
+            return cached[1]
+        tables = None
+        if self.n < 2**32:
+            t32 = torch.empty(seeds.numel(), dtype=torch.int32, device=seeds.device)
+            flag = torch.zeros(1, dtype=torch.int32, device=seeds.device)
+            nparts = self.num_partitions
+            _native.call("phb_seed_table32", _native.ptr(seeds), _native.ptr(key_off), nparts,
+                         seeds.numel(), _native.ptr(t32), _native.ptr(flag), _native.stream())
+            part2 = torch.empty(2 * nparts, dtype=torch.int32, device=seeds.device)
+            _native.call("phb_part_table32", _native.ptr(key_off), nparts, _native.ptr(part2),
+                         _native.stream())
+            if not int(flag.item()):
+                tables = (t32, part2)
+        self._tables32 = (seeds, tables)
+        return tables
+
     def query_device(self, keys) -> torch.Tensor:
         """Batched device query -> int64 CUDA tensor (query_many_kernel, _kernels.py:379-397)."""
         dev = _native.require_device()
@@ -391,6 +414,16 @@ class Mphf:
         dk = keys if isinstance(keys, DeviceKeys) else to_device(keys, dev)
         out = torch.empty(dk.n, dtype=torch.int64, device=dev)
         P = _native.ptr
+        tables = self._query_tables32(seeds, key_off)
+        if tables is not None and (not dk.is_u64 or dk.keys64.data_ptr() % 16 == 0):
+            t32, part2 = tables
+            _native.call("phb_query32", None if dk.is_u64 else P(dk.buf),
+                         None if dk.is_u64 else P(dk.offsets),
+                         P(dk.keys64) if dk.is_u64 else None, dk.n,
+                         self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n, self.num_partitions,
+                         P(key_off), P(part2), P(entries), self.bcount, P(t32), P(out),
+                         _native.stream())
+            return out
         _native.call("phb_query", None if dk.is_u64 else P(dk.buf),
                      None if dk.is_u64 else P(dk.offsets), P(dk.keys64) if dk.is_u64 else None,
                      dk.n, self.global_seed & 0xFFFFFFFFFFFFFFFF, self.n,
