@@ -98,8 +98,10 @@ int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
  * deltas[nparts+1] = key_base + key_off[j] - expected(part_base + j,
  * global_n, global_nparts) (partitioning.py:101-108); stats[0] = max |delta|,
  * stats[1] = max partition size. For a single-GPU build pass key_base =
- * part_base = 0, global_n = n, global_nparts = nparts. */
-int phb_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
+ * part_base = 0, global_n = n, global_nparts = nparts. counts (8-byte
+ * aligned) is CLOBBERED: the multi-CTA scan keeps its tile states over the
+ * tiles' first counts (no scratch allocation). */
+int phb_layout(uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
                int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                int64_t* stats, void* stream);
 

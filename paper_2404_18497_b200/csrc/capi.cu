@@ -13,6 +13,27 @@ namespace phb {
 
 unsigned long long g_launch_count = 0;
 
+// Stream-ordered scratch for the library's short-lived buffers (layout
+// tile states, decode temporaries, ...). The device's default memory pool
+// keeps freed blocks (release threshold raised once per device), so these
+// allocations do not go back to the driver at every synchronisation;
+// PyTorch's own allocator does not use this pool.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static int configured[64] = {0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64 && !__atomic_load_n(&configured[dev], __ATOMIC_ACQUIRE)) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 1ull << 30;  // up to 1 GiB of freed blocks stay in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    __atomic_store_n(&configured[dev], 1, __ATOMIC_RELEASE);
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+
 int num_sms() {
   static int cached[64] = {0};
   int dev = 0;
@@ -113,7 +134,7 @@ int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
   return launch_hash_count(buf, offsets, keys64, n, seed, (uint64_t)nparts, counts, S(stream));
 }
 
-int phb_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
+int phb_layout(uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
                int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                int64_t* stats, void* stream) {
   return launch_layout(counts, nparts, key_base, part_base, global_n, global_nparts, key_off,
@@ -215,7 +236,7 @@ int phb_build_partition_range(const uint64_t* his, const uint64_t* los, const in
   cudaStream_t st = S(stream);
   unsigned long long* d_stat = nullptr;
   unsigned long long h_stat[3] = {0, 0, 0};
-  PHB_CUDA_TRY(cudaMallocAsync(&d_stat, 3 * sizeof(unsigned long long), st));
+  PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&d_stat), 3 * sizeof(unsigned long long), st));
   PHB_CUDA_TRY(cudaMemsetAsync(d_stat, 0, 3 * sizeof(unsigned long long), st));
   int g = (int)std::min<int64_t>((p_hi - p_lo + 255) / 256, 1024);
   note_launch(), k_range_max<<<g, 256, 0, st>>>(key_off, p_lo, p_hi, d_stat);
@@ -227,9 +248,9 @@ int phb_build_partition_range(const uint64_t* his, const uint64_t* los, const in
   uint16_t* bid = nullptr;
   uint64_t* glo = nullptr;
   uint32_t* queue = nullptr;
-  PHB_CUDA_TRY(cudaMallocAsync(&bid, sizeof(uint16_t) * (nk > 0 ? nk : 1), st));
-  PHB_CUDA_TRY(cudaMallocAsync(&glo, sizeof(uint64_t) * (nk > 0 ? nk : 1), st));
-  PHB_CUDA_TRY(cudaMallocAsync(&queue, sizeof(uint32_t), st));
+  PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&bid), sizeof(uint16_t) * (nk > 0 ? nk : 1), st));
+  PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&glo), sizeof(uint64_t) * (nk > 0 ? nk : 1), st));
+  PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&queue), sizeof(uint32_t), st));
   int rc = launch_bucket_ids(his + k0, nk, entries, (uint32_t)bcount, bid, st);
   if (rc == 0) {
     SearchArgs a;
@@ -275,7 +296,7 @@ int phb_query_many(const uint64_t* his, const uint64_t* los, int64_t nq, int64_t
   if (nparts < 1) return PHB_E_ARGS;
   cudaStream_t st = S(stream);
   int64_t* key_off = nullptr;
-  PHB_CUDA_TRY(cudaMallocAsync(&key_off, sizeof(int64_t) * (nparts + 1), st));
+  PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&key_off), sizeof(int64_t) * (nparts + 1), st));
   int rc = phb_offsets_from_deltas(deltas, n, nparts, key_off, stream);
   if (rc == 0)
     rc = launch_query(nullptr, nullptr, nullptr, his, los, nq, 0, n, nparts, key_off, entries,

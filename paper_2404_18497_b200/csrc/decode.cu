@@ -198,7 +198,7 @@ int launch_decode(const uint8_t* blob, int64_t ncols, const int64_t* host_info, 
   DCol* dcols = nullptr;
   unsigned long long* csum = nullptr;
   uint64_t* pos = nullptr;
-  PHB_CUDA_TRY(cudaMallocAsync(&dcols, sizeof(DCol) * ncols, st));
+  PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&dcols), sizeof(DCol) * ncols, st));
   PHB_CUDA_TRY(cudaMemcpyAsync(dcols, host_info, sizeof(DCol) * ncols, cudaMemcpyHostToDevice, st));
   const int64_t total = ncols * per_col;
   int g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
@@ -206,8 +206,8 @@ int launch_decode(const uint8_t* blob, int64_t ncols, const int64_t* host_info, 
   note_launch(), k_decode_fields<<<g, 256, 0, st>>>(blob, dcols, ncols, per_col, nparts, B, mono, seeds);
   PHB_CUDA_TRY(cudaGetLastError());
   if (any_rice) {
-    PHB_CUDA_TRY(cudaMallocAsync(&csum, sizeof(unsigned long long) * ncols * nch, st));
-    PHB_CUDA_TRY(cudaMallocAsync(&pos, sizeof(uint64_t) * ncols * per_col, st));
+    PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&csum), sizeof(unsigned long long) * ncols * nch, st));
+    PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&pos), sizeof(uint64_t) * ncols * per_col, st));
     note_launch(), k_highs_chunks<<<(unsigned)(ncols * nch), DT, 0, st>>>(blob, dcols, nch, csum);
     note_launch(), k_highs_scan<<<(unsigned)((ncols + 255) / 256), 256, 0, st>>>(ncols, nch, csum);
     note_launch(), k_highs_emit<<<(unsigned)(ncols * nch), DT, 0, st>>>(blob, dcols, nch, csum, per_col, pos);

@@ -112,28 +112,40 @@ __device__ __forceinline__ uint64_t shifted_sum(const unsigned long long* st, in
   return s;
 }
 
-// E2: per-column parameters, block sizes and byte offsets; status / trials
-// reduction; seed-section geometry. One CTA.
+// E1b: status / trials reduction over the partitions, multi-CTA: trials
+// summed into sum->trials_total, the first failing partition j kept as
+// max(nparts - j) in sum->first_bad (0 = none; k_plan decodes it).
+// sum->trials_total and sum->first_bad are zeroed before the launch.
+__global__ void __launch_bounds__(256) k_status_reduce(const int64_t* __restrict__ part_trials,
+                                                       const uint8_t* __restrict__ status,
+                                                       int64_t nparts,
+                                                       EncodeSummary* __restrict__ sum) {
+  unsigned long long tr = 0, bad = 0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nparts;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (part_trials) tr += (unsigned long long)part_trials[j];
+    if (status && status[j]) bad = max(bad, (unsigned long long)(nparts - j));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    bad = max(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (tr) atomicAdd(reinterpret_cast<unsigned long long*>(&sum->trials_total), tr);
+    if (bad) atomicMax(reinterpret_cast<unsigned long long*>(&sum->first_bad), bad);
+  }
+}
+
+// E2: per-column parameters, block sizes and byte offsets; seed-section
+// geometry. One CTA (the partition-wide reduction is k_status_reduce).
 __global__ void __launch_bounds__(1024) k_plan(EncodeArgs a, const unsigned long long* colstat,
                                                ColInfo* __restrict__ info,
                                                EncodeSummary* __restrict__ sum) {
   __shared__ unsigned long long sh[32];
-  __shared__ unsigned long long s_trials;
-  __shared__ int s_bad;
   const int ncols = a.mono ? 1 : (int)a.bcount;
   const int64_t cnt = a.count_global ? a.count_global
                                      : (a.mono ? a.nparts * (int64_t)a.bcount : a.nparts);
-  if (threadIdx.x == 0) s_trials = 0, s_bad = 0x7fffffff;
-  __syncthreads();
-  // status / trials over partitions
-  unsigned long long tr = 0;
-  int bad = 0x7fffffff;
-  for (int64_t j = threadIdx.x; j < a.nparts; j += blockDim.x) {
-    if (a.part_trials) tr += (unsigned long long)a.part_trials[j];
-    if (a.status && a.status[j] && j < bad) bad = (int)j;
-  }
-  atomicAdd(&s_trials, tr);
-  atomicMin(&s_bad, bad);
 
   // delta width (partitioning.py:125-128): bitlen(max |delta|) + 1
   const int w = bitlen64((uint64_t)a.layout_stats[0]) + 1;
@@ -223,9 +235,10 @@ __global__ void __launch_bounds__(1024) k_plan(EncodeArgs a, const unsigned long
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    sum->trials_total = s_trials;
-    sum->first_bad = s_bad == 0x7fffffff ? -1 : s_bad;
-    sum->bad_code = (s_bad == 0x7fffffff || !a.status) ? 0 : a.status[s_bad];
+    const int64_t v = sum->first_bad;  // max(nparts - j) from k_status_reduce, 0 = none
+    const int64_t bad = v ? a.nparts - v : -1;
+    sum->first_bad = bad;
+    sum->bad_code = (bad < 0 || !a.status) ? 0 : a.status[bad];
     sum->ncols = ncols;
   }
 }
@@ -426,6 +439,13 @@ int launch_encode_plan(const EncodeArgs& a, void* ws, EncodeSummary* host_sum, c
   } else {
     PHB_CUDA_TRY(cudaMemsetAsync(L.colstat, 0, (size_t)ncols * 65 * 8, st));
     note_launch(), k_col_stats<<<(unsigned)(ncols * nch), ET, 0, st>>>(cols, nch, L.colstat);
+    PHB_CUDA_TRY(cudaGetLastError());
+  }
+  PHB_CUDA_TRY(cudaMemsetAsync(L.sum, 0, sizeof(EncodeSummary), st));
+  if (a.nparts > 0 && (a.part_trials || a.status)) {
+    const int64_t g = std::min<int64_t>(cdiv(a.nparts, 256), (int64_t)num_sms() * 4);
+    note_launch(), k_status_reduce<<<(unsigned)g, 256, 0, st>>>(a.part_trials, a.status,
+                                                                a.nparts, L.sum);
     PHB_CUDA_TRY(cudaGetLastError());
   }
   note_launch(), k_plan<<<1, 1024, 0, st>>>(a, L.colstat, L.info, L.sum);

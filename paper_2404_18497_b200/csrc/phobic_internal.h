@@ -16,6 +16,7 @@ inline int note_launch() {
 }
 
 int num_sms();
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
 
 int launch_murmur(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
                   uint64_t seed, uint64_t* hi, uint64_t* lo, cudaStream_t st);
@@ -41,7 +42,7 @@ size_t layout_temp_bytes(int64_t nparts);
 // expected offsets of the global layout: global_n / global_nparts, shifted
 // by part_base / key_base for sharded builds), stats[0] = max |delta|,
 // stats[1] = max partition size.
-int launch_layout(const uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
+int launch_layout(uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
                   int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                   int64_t* stats, void* temp, size_t temp_bytes, cudaStream_t st);
 

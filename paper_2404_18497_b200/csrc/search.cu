@@ -504,11 +504,14 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     for (int t = 0; t < WPL; ++t) sat &= acc[t];
     const bool hv = sat != FULL && !(G > 1 && gcoll);
     const uint32_t fball = __ballot_sync(FULL, hv);
-    int64_t myd = -1;
-    if (hv) {
+    // this lane's first free displacement, 32-bit (only a lane with hv is read)
+    uint32_t myd = 0;
+    if (fball) {
+      uint32_t tw = 0, vv = FULL;
 #pragma unroll
       for (int t = WPL - 1; t >= 0; --t)
-        if (acc[t] != FULL) myd = 32 * (int64_t)(wb + t) + (__ffs(~acc[t]) - 1);
+        if (acc[t] != FULL) tw = (uint32_t)t, vv = acc[t];
+      myd = 32u * (wb + tw) + (uint32_t)(__ffs(~vv) - 1);
     }
     if constexpr (G > 1) {
       // closed form of the sequential loop: seeds before the first group with
@@ -766,8 +769,12 @@ int launch_search(const SearchArgs& a, cudaStream_t st) {
   // the device's opt-in maximum, not this launch's size: host threads
   // launching concurrently (compat_kernels under builder.py's thread pool)
   // would otherwise race on the attribute and launch above each other's cap
+  cudaFuncAttributes fa;
+  PHB_CUDA_TRY(cudaFuncGetAttributes(&fa, k_search));
+  const int dyn_max = max_optin - (int)fa.sharedSizeBytes;  // the static part counts too
+  if (per_cta > (size_t)dyn_max) return 1002;               // PHB_E_PARTITION_TOO_LARGE
   PHB_CUDA_TRY(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    max_optin));
+                                    dyn_max));
   int per_sm = 0;
   PHB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, WARPS * 32,
                                                              per_cta));

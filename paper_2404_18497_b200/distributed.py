@@ -239,7 +239,7 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
         dist.all_gather(gathered, counts, group=group)
         C = torch.stack(gathered).to(torch.int64)            # [G, nparts]
         total_counts = C.sum(0).to(torch.int32)
-        key_off_g, deltas, stats = ops.layout(total_counts, n, nparts)
+        key_off_g, deltas, stats = ops.layout(total_counts.clone(), n, nparts)  # clobbers counts
         C_owned = C[:, p_lo:p_hi]
         # one small host read: every rank's receive count and the owned max size
         bt = torch.tensor(bounds, device=C.device)

@@ -196,3 +196,31 @@ def test_search_vs_oracle_random(nat, orc, lam, P, n):
         assert np.array_equal(status, wst)
         assert np.array_equal(seeds, ws)
         assert np.array_equal(trials, wt)
+
+
+@pytest.mark.parametrize("nparts", [1, 2, 3, 4095, 4096, 4097, 8192, 123_457, 600_000])
+def test_layout_multi_tile(nat, nparts):
+    """K2's multi-CTA scan (tiles of 4096 partitions, decoupled look-back)
+    against numpy, at tile boundaries and at 147 tiles, with a shard offset
+    (key_base / part_base as the multi-GPU owner ranges pass them)."""
+    rng = np.random.default_rng(nparts)
+    counts_np = rng.integers(0, 5000, size=nparts).astype(np.int64)
+    part_base = nparts // 3
+    gnparts = nparts + part_base + 7
+    key_base = int(rng.integers(0, 1_000_000))
+    gn = int(counts_np.sum()) + key_base + 12345
+    counts = torch.from_numpy(counts_np.astype(np.int32)).to(DEV)
+    key_off = torch.empty(nparts + 1, dtype=torch.int64, device=DEV)
+    deltas = torch.empty_like(key_off)
+    stats = torch.empty(2, dtype=torch.int64, device=DEV)
+    nat.call("phb_layout", nat.ptr(counts), nparts, key_base, part_base, gn, gnparts,
+             nat.ptr(key_off), nat.ptr(deltas), nat.ptr(stats), nat.stream())
+    want_off = np.zeros(nparts + 1, np.int64)
+    np.cumsum(counts_np, out=want_off[1:])
+    j = np.arange(nparts + 1, dtype=object) + part_base
+    expected = np.array((2 * j * gn + gnparts) // (2 * gnparts), dtype=np.int64)
+    want_d = key_base + want_off - expected
+    assert np.array_equal(key_off.cpu().numpy(), want_off)
+    assert np.array_equal(deltas.cpu().numpy(), want_d)
+    st = stats.cpu().numpy()
+    assert st[0] == np.abs(want_d).max() and st[1] == counts_np.max()
