@@ -573,6 +573,151 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   return {0, trials, -1};
 }
 
+// Speculative seed-0 step for up to four consecutive small buckets
+// (2 <= k <= 8) of the processing order, one 8-lane group each (the
+// small_bucket<4> layout: 12 words of the valid mask per lane). Every group
+// sweeps seed 0 against the occupancy before the step; the groups are then
+// accepted in order: group g keeps its first-fit displacement d_g if it has
+// one (and no self-collision) and none of its slots was taken by the
+// groups accepted before it in this step. That is exactly the sequential
+// result: displacements below d_g were invalid on the old occupancy and
+// stay invalid with more slots taken (_kernels.py:312-369; trials k (d + 1)).
+// The first group that fails ends the step; its bucket (and the rest) go
+// on through the regular path. Returns the number of buckets placed and
+// writes their seeds / trials; *tr_out accumulates their trials.
+__device__ uint32_t multi_bucket0(const SearchArgs& a, int64_t row, uint32_t occ, uint32_t dmask,
+                                  uint16_t* pos16, const uint16_t* order, uint32_t oi, uint32_t nG,
+                                  uint32_t cnt, uint32_t endp, const uint64_t* kbase, uint32_t m,
+                                  uint64_t g0, int64_t& tr_out, uint32_t& placed, int lane) {
+  constexpr int L = 8, WPL = 12;
+  const int grp = lane >> 3, gl = lane & 7;
+  const bool ing = (uint32_t)grp < nG;
+  const uint32_t bg = ing ? order[oi + grp] : 0u;
+  const uint32_t kg = ing ? smem[cnt + bg] : 0u;
+  const bool act = (uint32_t)gl < kg;
+  const uint64_t key = act ? kbase[smem[endp + bg] - kg + gl] : 0ull;
+  const uint32_t p = position(key, g0, m);
+  const uint32_t tag = act ? (((uint32_t)grp << 16) | p) : (0x80000000u | (uint32_t)lane);
+  const uint32_t tpeers = __match_any_sync(FULL, tag);
+  const uint32_t cball = __ballot_sync(FULL, act && __popc(tpeers) > 1);
+  // base positions, every group padded to the largest k (pairs) with its last key
+  const uint32_t kmax = __reduce_max_sync(FULL, kg);
+  const uint32_t kpad = (kmax + 1u) & ~1u;
+  const uint32_t from = kg ? (uint32_t)(grp * L) + min((uint32_t)gl, kg - 1u) : (uint32_t)lane;
+  const uint32_t pfill = __shfl_sync(FULL, p, from);
+  uint16_t* const mypos = pos16 + grp * L;
+  if ((uint32_t)gl < kpad) mypos[gl] = (uint16_t)pfill;
+  __syncwarp();
+  const uint32_t wb = (uint32_t)gl * WPL;
+  uint32_t acc[WPL];
+#pragma unroll
+  for (int t = 0; t < WPL; ++t) acc[t] = smem[dmask + wb + t];
+  const uint32_t* const mp32 = reinterpret_cast<const uint32_t*>(mypos);
+#pragma unroll 1
+  for (uint32_t i = 0; i < kpad; i += 2) {
+    const uint32_t pp = mp32[i >> 1];
+    const uint32_t pa = pp & 0xffffu, pb = pp >> 16;
+    const uint32_t sa = pa & 31, sb = pb & 31;
+    const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
+    uint32_t xa = smem[Wa], xb = smem[Wb];
+#pragma unroll
+    for (int t = 0; t < WPL; ++t) {
+      const uint32_t ya = smem[Wa + t + 1], yb = smem[Wb + t + 1];
+      acc[t] |= __funnelshift_r(xa, ya, sa) | __funnelshift_r(xb, yb, sb);
+      xa = ya;
+      xb = yb;
+    }
+  }
+  uint32_t sat = FULL;
+#pragma unroll
+  for (int t = 0; t < WPL; ++t) sat &= acc[t];
+  const bool gcoll = ((cball >> (grp * L)) & 0xffu) != 0;
+  const uint32_t fball = __ballot_sync(FULL, ing && sat != FULL && !gcoll);
+  uint32_t myd = 0;
+  if (fball) {
+    uint32_t tw = 0, vv = FULL;
+#pragma unroll
+    for (int t = WPL - 1; t >= 0; --t)
+      if (acc[t] != FULL) tw = (uint32_t)t, vv = acc[t];
+    myd = 32u * (wb + tw) + (uint32_t)(__ffs(~vv) - 1);
+  }
+  uint32_t accepted = 0;
+#pragma unroll 1
+  for (uint32_t g = 0; g < nG; ++g) {
+    const uint32_t gb = (fball >> (g * L)) & 0xffu;
+    if (!gb) break;  // no fit at seed 0, or a self-collision: the regular path decides
+    const uint32_t d = __shfl_sync(FULL, myd, (int)(g * L) + __ffs(gb) - 1);
+    uint32_t slot = p + d;
+    if (slot >= m) slot -= m;
+    const bool mine = (uint32_t)grp == g && act;
+    const bool taken = mine && ((smem[occ + (slot >> 5)] >> (slot & 31)) & 1u);
+    if (__any_sync(FULL, taken)) break;  // collides with a group placed in this step
+    if (mine) mark(occ, slot, m, 500 + (int)kg);
+    __syncwarp();
+    const uint32_t kgg = __shfl_sync(FULL, kg, (int)(g * L));
+    const uint32_t bgg = __shfl_sync(FULL, bg, (int)(g * L));
+    const int64_t tr = (int64_t)kgg * ((int64_t)d + 1);
+    if (lane == 0) {
+      a.seeds[row * a.s_sj + (int64_t)(bgg - 1) * a.s_sb] = (uint64_t)d;
+      if (a.trials) a.trials[row * a.s_sj + (int64_t)(bgg - 1) * a.s_sb] = tr;
+    }
+    tr_out += tr;
+    placed += kgg;
+    ++accepted;
+  }
+  return accepted;
+}
+
+// The trailing singletons (k = 1 buckets come last in the size-descending
+// order), up to 32 per step, one per lane: a singleton takes the first
+// free slot cyclically from its seed-0 base (_kernels.py:300-310). Lanes
+// resolve in lane order: every round, the unresolved lanes scan the current
+// occupancy, the longest prefix of them with pairwise distinct slots is
+// placed (a lower lane's slot can only change a higher lane's first free
+// slot by being that very slot), the rest scan again.
+__device__ void singles0(const SearchArgs& a, int64_t row, uint32_t occ, const uint16_t* order,
+                         uint32_t oi, uint32_t nS, uint32_t endp, const uint64_t* kbase,
+                         uint32_t m, uint64_t g0, int64_t& tr_out, int lane) {
+  const bool act = (uint32_t)lane < nS;
+  const uint32_t b = act ? order[oi + lane] : 0u;
+  const uint64_t key = act ? kbase[smem[endp + b] - 1] : 0ull;
+  const uint32_t p = position(key, g0, m);
+  uint32_t unresolved = nS >= 32 ? FULL : ((1u << nS) - 1u);
+  uint32_t slot = 0;
+#pragma unroll 1
+  while (unresolved) {
+    const bool mine = (unresolved >> lane) & 1u;
+    if (mine) {
+      // first free bit at or after p in the doubled bitmap (one exists in [p, p + m))
+      uint32_t w = p >> 5;
+      uint32_t bits = ~smem[occ + w] & (FULL << (p & 31));
+#pragma unroll 1
+      while (!bits) bits = ~smem[occ + (++w)];
+      slot = 32u * w + (uint32_t)(__ffs(bits) - 1);
+      if (slot >= m) slot -= m;
+    }
+    const uint32_t tag = mine ? slot : (0x80000000u | (uint32_t)lane);
+    const uint32_t peers = __match_any_sync(FULL, tag);
+    const uint32_t clash = __ballot_sync(FULL, mine && (peers & lanemask_lt() & unresolved) != 0u);
+    const uint32_t now = unresolved & (clash ? (clash & (0u - clash)) - 1u : FULL);
+    if ((now >> lane) & 1u) mark(occ, slot, m, 1);
+    __syncwarp();
+    unresolved &= ~now;
+  }
+  const uint32_t d = act ? (slot >= p ? slot - p : slot + m - p) : 0u;
+  if (act) {
+    a.seeds[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = (uint64_t)d;
+    if (a.trials) a.trials[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = (int64_t)d + 1;
+  }
+  tr_out += (int64_t)__reduce_add_sync(FULL, act ? d + 1u : 0u);
+}
+
+// LOWL (low lambda, average bucket below ~7 keys): most buckets fit at seed 0,
+// so the per-bucket fixed cost dominates; the trailing singletons go 32 per
+// step (singles0) and runs of small buckets 4 per speculative seed-0 step
+// (multi_bucket0). A separate instantiation, so the high-lambda kernel keeps
+// its instruction footprint (measured: both paths cost ~3% at lambda = 9).
+template <bool LOWL>
 __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, SmemPlan plan) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t B = a.bcount;
@@ -671,15 +816,53 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     int64_t ptrials = 0;
     uint8_t status = 0;
     const bool small_ok = m <= 3072;
+    // speculative seed-0 steps over several small buckets pay while most of
+    // them fit at seed 0, i.e. below ~85% fill; they need the whole seed-0
+    // displacement range below the cap
+    const bool multi_ok = small_ok && cap >= (int64_t)m - 1;
+    uint32_t placed = 0, mb_fail = 0xffffffffu;
 #pragma unroll 1
-    for (uint32_t oi = 0; oi < nb; ++oi) {
+    for (uint32_t oi = 0; oi < nb;) {
       const uint32_t b = order[oi];
       const uint32_t k = smem[cnt + b];
       const uint64_t* kl = a.glo + kb + (smem[endp + b] - k);
       BucketResult res;
       STAT(k == 1 ? 6 : 7, 1);
       TSTAMP(tb);
-      if (k == 1) {
+      if (LOWL && k == 1) {
+        // the trailing singletons, up to 32 per step (no cap: _kernels.py:300-310)
+        const uint32_t nS = min(32u, nb - oi);
+        singles0(a, row, occ, order, oi, nS, endp, a.glo + kb, m, g0, ptrials, lane);
+        TACC(11, tb);
+        oi += nS;
+        continue;
+      }
+#ifndef PHB_MB_E
+#define PHB_MB_E 4.0f
+#endif
+      // expected seed-0 fits of this bucket, m (1 - fill)^k: the step pays
+      // when the first (largest) bucket almost surely fits at seed 0
+      if (LOWL && multi_ok && k <= 8 && oi != mb_fail && oi + 1 < nb &&
+          (float)m * __powf((float)(m - placed) / (float)m, (float)k) >= PHB_MB_E) {
+        uint32_t nG = 1;
+#pragma unroll 1
+        while (nG < 4 && oi + nG < nb) {
+          const uint32_t kn = smem[cnt + order[oi + nG]];
+          if (kn < 2) break;
+          ++nG;
+        }
+        if (nG >= 2) {
+          const uint32_t acc_n = multi_bucket0(a, row, occ, dmask, pos16, order, oi, nG, cnt, endp,
+                                               a.glo + kb, m, g0, ptrials, placed, lane);
+          TACC(12, tb);
+          if (acc_n) {
+            oi += acc_n;
+            continue;
+          }
+          mb_fail = oi;  // this bucket failed seed 0: the regular path takes it
+        }
+      }
+      if (!LOWL && k == 1) {
         // singleton: first free slot cyclically from the s = 0 base; no cap
         // (_kernels.py:300-310)
         const uint32_t p = position(kl[0], g0, m);
@@ -731,6 +914,8 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
         if (a.trials) a.trials[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = res.trials;
       }
       ptrials += res.trials;
+      placed += k;
+      ++oi;
     }
     __syncwarp();
     if (lane == 0) {
@@ -769,21 +954,27 @@ int launch_search(const SearchArgs& a, cudaStream_t st) {
   // the device's opt-in maximum, not this launch's size: host threads
   // launching concurrently (compat_kernels under builder.py's thread pool)
   // would otherwise race on the attribute and launch above each other's cap
+  // average keys per bucket, from the largest partition: below 6 the
+  // low-lambda instantiation (measured at C2: lambda = 4 / 5 search 10.6 /
+  // 9.3 -> 7.9 / 7.5 ms; at lambda = 6 and up it is slower)
+  const bool lowl = (double)a.m_max < 6.0 * (double)a.bcount;
+  const void* fn = lowl ? (const void*)k_search<true> : (const void*)k_search<false>;
   cudaFuncAttributes fa;
-  PHB_CUDA_TRY(cudaFuncGetAttributes(&fa, k_search));
+  PHB_CUDA_TRY(cudaFuncGetAttributes(&fa, fn));
   const int dyn_max = max_optin - (int)fa.sharedSizeBytes;  // the static part counts too
   if (per_cta > (size_t)dyn_max) return 1002;               // PHB_E_PARTITION_TOO_LARGE
-  PHB_CUDA_TRY(cudaFuncSetAttribute(k_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    dyn_max));
+  PHB_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max));
   int per_sm = 0;
-  PHB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_search, WARPS * 32,
-                                                             per_cta));
+  PHB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, per_cta));
   if (per_sm < 1) per_sm = 1;
   int64_t want = (nrange + WARPS - 1) / WARPS;
   int64_t cap = (int64_t)num_sms() * per_sm;
   int grid = (int)(want < cap ? want : cap);
   PHB_CUDA_TRY(cudaMemsetAsync(a.queue, 0, sizeof(uint32_t), st));
-  note_launch(), k_search<<<grid, WARPS * 32, per_cta, st>>>(a, plan);
+  if (lowl)
+    note_launch(), k_search<true><<<grid, WARPS * 32, per_cta, st>>>(a, plan);
+  else
+    note_launch(), k_search<false><<<grid, WARPS * 32, per_cta, st>>>(a, plan);
   return (int)cudaGetLastError();
 }
 
