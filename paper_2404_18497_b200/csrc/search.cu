@@ -669,47 +669,47 @@ __device__ uint32_t multi_bucket0(const SearchArgs& a, int64_t row, uint32_t occ
 }
 
 // The trailing singletons (k = 1 buckets come last in the size-descending
-// order), up to 32 per step, one per lane: a singleton takes the first
-// free slot cyclically from its seed-0 base (_kernels.py:300-310). Lanes
-// resolve in lane order: every round, the unresolved lanes scan the current
-// occupancy, the longest prefix of them with pairwise distinct slots is
-// placed (a lower lane's slot can only change a higher lane's first free
-// slot by being that very slot), the rest scan again.
-__device__ void singles0(const SearchArgs& a, int64_t row, uint32_t occ, const uint16_t* order,
-                         uint32_t oi, uint32_t nS, uint32_t endp, const uint64_t* kbase,
-                         uint32_t m, uint64_t g0, int64_t& tr_out, int lane) {
+// order), up to 32 per step: a singleton takes the first free slot
+// cyclically from its seed-0 base (_kernels.py:300-310), in order. The
+// lanes hash the keys in parallel; lane 0 then places them one after the
+// other with word scans of the doubled bitmap (a singleton costs ~15
+// instructions: the few issue slots of this latency-bound loop leave the
+// SM to the other warps). Seeds and trials are written by the lanes.
+__device__ void singles0(const SearchArgs& a, int64_t row, uint32_t occ, uint16_t* pos16,
+                         const uint16_t* order, uint32_t oi, uint32_t nS, uint32_t endp,
+                         const uint64_t* kbase, uint32_t m, uint64_t g0, int64_t& tr_out,
+                         int lane) {
   const bool act = (uint32_t)lane < nS;
   const uint32_t b = act ? order[oi + lane] : 0u;
   const uint64_t key = act ? kbase[smem[endp + b] - 1] : 0ull;
   const uint32_t p = position(key, g0, m);
-  uint32_t unresolved = nS >= 32 ? FULL : ((1u << nS) - 1u);
-  uint32_t slot = 0;
+  if (act) pos16[lane] = (uint16_t)p;
+  __syncwarp();
+  if (lane == 0) {
 #pragma unroll 1
-  while (unresolved) {
-    const bool mine = (unresolved >> lane) & 1u;
-    if (mine) {
-      // first free bit at or after p in the doubled bitmap (one exists in [p, p + m))
-      uint32_t w = p >> 5;
-      uint32_t bits = ~smem[occ + w] & (FULL << (p & 31));
+    for (uint32_t i = 0; i < nS; ++i) {
+      const uint32_t q = pos16[i];
+      // first free bit at or after q in the doubled bitmap (one exists in [q, q + m))
+      uint32_t w = q >> 5;
+      uint32_t bits = ~smem[occ + w] & (FULL << (q & 31));
 #pragma unroll 1
       while (!bits) bits = ~smem[occ + (++w)];
-      slot = 32u * w + (uint32_t)(__ffs(bits) - 1);
+      uint32_t slot = 32u * w + (uint32_t)(__ffs(bits) - 1);
       if (slot >= m) slot -= m;
+      smem[occ + (slot >> 5)] |= 1u << (slot & 31);  // one writer: plain stores
+      const uint32_t s2 = slot + m;
+      smem[occ + (s2 >> 5)] |= 1u << (s2 & 31);
+      pos16[i] = (uint16_t)(slot >= q ? slot - q : slot + m - q);  // d
     }
-    const uint32_t tag = mine ? slot : (0x80000000u | (uint32_t)lane);
-    const uint32_t peers = __match_any_sync(FULL, tag);
-    const uint32_t clash = __ballot_sync(FULL, mine && (peers & lanemask_lt() & unresolved) != 0u);
-    const uint32_t now = unresolved & (clash ? (clash & (0u - clash)) - 1u : FULL);
-    if ((now >> lane) & 1u) mark(occ, slot, m, 1);
-    __syncwarp();
-    unresolved &= ~now;
   }
-  const uint32_t d = act ? (slot >= p ? slot - p : slot + m - p) : 0u;
+  __syncwarp();
+  const uint32_t d = act ? (uint32_t)pos16[lane] : 0u;
   if (act) {
     a.seeds[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = (uint64_t)d;
     if (a.trials) a.trials[row * a.s_sj + (int64_t)(b - 1) * a.s_sb] = (int64_t)d + 1;
   }
   tr_out += (int64_t)__reduce_add_sync(FULL, act ? d + 1u : 0u);
+  __syncwarp();
 }
 
 // LOWL (low lambda, average bucket below ~7 keys): most buckets fit at seed 0,
@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
       if (LOWL && k == 1) {
         // the trailing singletons, up to 32 per step (no cap: _kernels.py:300-310)
         const uint32_t nS = min(32u, nb - oi);
-        singles0(a, row, occ, order, oi, nS, endp, a.glo + kb, m, g0, ptrials, lane);
+        singles0(a, row, occ, pos16, order, oi, nS, endp, a.glo + kb, m, g0, ptrials, lane);
         TACC(11, tb);
         oi += nS;
         continue;
