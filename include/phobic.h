@@ -107,14 +107,16 @@ int phb_layout(uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_
 
 /* K3: re-hash and scatter (lo, bucket id) into partition ranges (cursor:
  * nparts u32 of scratch, contents ignored; n < 2^32). Replaces the lexsort grouping (partitioning.py:93-95)
- * and _bucket_of (_kernels.py:252-255). */
+ * and _bucket_of (_kernels.py:252-255). bid_out == NULL: 16-byte records
+ * {lo, bucket id} into lo_out (2n u64), one scattered store per key. */
 int phb_scatter(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
                 uint64_t seed, int64_t nparts, const double* entries, int32_t bcount,
                 const int64_t* key_off, uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,
                 void* stream);
 
 /* K4: bucket order + seed search for partitions [p_lo, p_hi) over records
- * grouped by partition. Seeds land at seeds[(j-out_base)*s_sj + (b-1)*s_sb];
+ * grouped by partition (separate lo / bid arrays, or bid == NULL: lo holds
+ * the 16-byte {lo, bucket id} records of phb_scatter). Seeds land at seeds[(j-out_base)*s_sj + (b-1)*s_sb];
  * trials (may be NULL) at the same index; part_trials[(j-out_base)] (may be
  * NULL); status[(j-out_base)]. glo: scratch indexed like lo. queue: one
  * device u32. m_max: largest partition size in the range (layout stats[1]). */
@@ -126,7 +128,8 @@ int phb_search(const uint64_t* lo, const uint16_t* bid, const int64_t* key_off, 
 
 /* K3 into fixed-capacity partition slots, for u64 keys arriving in chunks
  * (no counting pass first): partition j's records go to [j*cap, j*cap + cap)
- * of lo_out / bid_out through cursor[j] (init != 0 on the first chunk sets
+ * of lo_out / bid_out (bid_out == NULL: 16-byte records in lo_out, as for
+ * phb_scatter) through cursor[j] (init != 0 on the first chunk sets
  * cursor[j] = j*cap; nparts*cap < 2^32). phb_padded_counts then turns the
  * cursors into the exact per-partition counts (input of phb_layout) and sets
  * *overflow if any partition exceeded cap (records past it are dropped: the

@@ -772,8 +772,12 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
 #pragma unroll 1
     for (uint32_t b = lane; b <= B; b += 32) smem[cnt + b] = 0;
     __syncwarp();
+    // records: separate (lo, u16 bucket id) arrays, or 16-byte (lo, bucket id)
+    // records when bid is null (phb_scatter's one-store layout)
+    const uint64_t* const rec = a.bid ? nullptr : a.lo;
 #pragma unroll 1
-    for (uint32_t q = lane; q < m; q += 32) atomicAdd(&smem[cnt + a.bid[kb + q]], 1u);
+    for (uint32_t q = lane; q < m; q += 32)
+      atomicAdd(&smem[cnt + (rec ? (uint32_t)rec[2 * (kb + q) + 1] : (uint32_t)a.bid[kb + q])], 1u);
     __syncwarp();
     uint32_t run = 0, maxsz = 0;
 #pragma unroll 1
@@ -789,9 +793,18 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     __syncwarp();
 #pragma unroll 1
     for (uint32_t q = lane; q < m; q += 32) {
-      const uint32_t b = a.bid[kb + q];
+      uint64_t lo;
+      uint32_t b;
+      if (rec) {
+        const ulonglong2 r = reinterpret_cast<const ulonglong2*>(rec)[kb + q];
+        lo = r.x;
+        b = (uint32_t)r.y;
+      } else {
+        lo = a.lo[kb + q];
+        b = a.bid[kb + q];
+      }
       const uint32_t at = atomicAdd(&smem[endp + b], 1u);
-      a.glo[kb + at] = a.lo[kb + q];
+      a.glo[kb + at] = lo;
     }
     const uint32_t occ_used = min((uint32_t)plan.occ_w, (2 * m) / 32 + 104);
 #pragma unroll 1

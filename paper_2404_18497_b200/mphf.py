@@ -142,8 +142,9 @@ class BuildEngine:
         P = _native.ptr
         L = _native.lib()
         cursor = torch.empty(nparts, dtype=torch.int32, device=dev)
-        lo = torch.empty(nparts * cap, dtype=torch.int64, device=dev)
-        bid = torch.empty(nparts * cap, dtype=torch.int16, device=dev)
+        # 16-byte (lo, bucket id) records: one scattered store per key
+        lo = torch.empty(2 * nparts * cap, dtype=torch.int64, device=dev)
+        bid = None
         flag = torch.zeros(1, dtype=torch.int32, device=dev)
         base = P(dk.keys64)
         cur = torch.cuda.current_stream(dev)
@@ -223,9 +224,15 @@ class BuildEngine:
         self._pinned.copy_(stats, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        # counts is reused as the scatter cursors (phb_scatter initialises them)
-        lo = torch.empty(n, dtype=torch.int64, device=dev)
-        bid = torch.empty(n, dtype=torch.int16, device=dev)
+        # counts is reused as the scatter cursors (phb_scatter initialises them);
+        # 16-byte (lo, bucket id) records (one scattered store per key) unless
+        # the instrumented build needs the bucket ids on their own
+        if instrument:
+            lo = torch.empty(n, dtype=torch.int64, device=dev)
+            bid = torch.empty(n, dtype=torch.int16, device=dev)
+        else:
+            lo = torch.empty(2 * n, dtype=torch.int64, device=dev)
+            bid = None
         _native.check(L.phb_scatter(buf, offs, k64, n, seed, nparts, P(self.entries), B,
                                     P(key_off), P(counts), P(lo), P(bid), st), "phb_scatter")
         seeds = torch.zeros(B * nparts, dtype=torch.int64, device=dev)
