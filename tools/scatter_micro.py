@@ -10,6 +10,7 @@ from paper_2404_18497_b200.assignment import tabulate
 from paper_2404_18497_b200.keygen import synth_u64_device
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+RECORDS = "--arrays" not in sys.argv  # default: the build's 16-byte record layout
 cfg = phb.BuildConfig(lambda_=9.0, partition_size=2500.0, encoder="ic-c")
 dev = torch.device("cuda", 0)
 keys = synth_u64_device(n, 0)
@@ -31,6 +32,6 @@ for r in range(6):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     _native.check(L.phb_scatter(None, None, P(keys), n, 0, nparts, P(entries), B, P(key_off),
-                                P(cur), P(lo), P(bid), st), "sc")
+                                P(cur), P(lo), None if RECORDS else P(bid), st), "sc")
     e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
 print("scatter ms", [round(t, 3) for t in ts])
