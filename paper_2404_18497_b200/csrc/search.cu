@@ -682,6 +682,7 @@ __device__ uint32_t multi_bucket0(const SearchArgs& a, int64_t row, uint32_t occ
     placed += kgg;
     ++accepted;
   }
+  __syncwarp();  // the sweep's reads of the base positions precede the next writer's
   return accepted;
 }
 

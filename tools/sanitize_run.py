@@ -15,6 +15,12 @@ for enc, lam, P in (("ic-c", 9.0, 2500.0), ("ic-r", 5.0, 300.0), ("mono-r", 7.0,
     assert torch.equal(f.query_encoded_device(dk), f.query_device(dk))
     g = phb.Mphf.deserialize(f.serialize())
     assert torch.equal(g.query_device(dk), f.query_device(dk))
+# multi-tile layout (10k partitions), the low-lambda search kernel, and the
+# shared-memory query path (>= 148 * 4096 u64 keys)
+big = np.unique(rng.integers(0, 2**64, size=1_000_000, dtype=np.uint64))
+f = phb.build(big, phb.BuildConfig(lambda_=4.0, partition_size=100.0, encoder="ic-c"))
+db = torch.from_numpy(big.view(np.int64)).cuda()
+assert f.verify_device(f.query_device(db))
 corpus = phb.gen_keys(5000, 3)
 f = phb.build(corpus, phb.BuildConfig(lambda_=8.0, partition_size=500.0))
 assert f.is_bijection_on(corpus)
