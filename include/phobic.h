@@ -285,7 +285,9 @@ int phb_regroup(const uint64_t* lo_in, const uint16_t* aux_in, const int32_t* co
  * part_base[j] + (rank of the key among this source's keys of partition j).
  * part_base: device i64[nparts]; owner: device u8[nparts] (owner rank of
  * partition j); lo_dst / bid_dst: HOST arrays of G device pointers (peer
- * buffers mapped with phb_ipc_open, the local one for g == rank); cursor:
+ * buffers mapped with phb_ipc_open, the local one for g == rank; bid_dst
+ * NULL: lo_dst buffers take 16-byte {lo, bucket id} records, one peer store
+ * per key, the layout phb_search reads with bid NULL); cursor:
  * device u32[nparts] scratch. The caller orders the kernel before the
  * owners' reads (stream sync + group barrier). */
 int phb_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,

@@ -490,7 +490,7 @@ int phb_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_t* 
                     const int64_t* part_base, const uint8_t* owner, uint64_t* const* lo_dst,
                     uint16_t* const* bid_dst, int32_t G, uint32_t* cursor, void* stream) {
   if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
-  if (!lo_dst || !bid_dst) return PHB_E_ARGS;
+  if (!lo_dst) return PHB_E_ARGS;  // bid_dst NULL: 16-byte records in lo_dst
   return launch_scatter_p2p(buf, offsets, keys64, n, seed, nparts, entries, (uint32_t)bcount,
                             part_base, owner, lo_dst, bid_dst, G, cursor, S(stream));
 }

@@ -5,7 +5,8 @@
 // exact slot range its records of partition j occupy inside the owner
 // rank's receive buffer (rank order inside a partition). The kernel hashes
 // each local key once, computes its bucket id, and stores (lo, bucket id)
-// straight into the owner's buffer through a CUDA-IPC-mapped peer pointer:
+// -- one 16-byte record per key when bid_dst is NULL, the layout the build
+// uses -- straight into the owner's buffer through a CUDA-IPC-mapped peer pointer:
 // the records land partition-grouped, so the owner runs K4 on them with no
 // receive-side regroup and no staging copy. Peer stores over NVLink 5 /
 // NVSwitch overlap the hashing of the next keys; the host orders the
@@ -22,7 +23,7 @@ struct PeerTable {
   uint16_t* bid[64];
 };
 
-template <class K>
+template <class K, bool REC>
 __global__ void __launch_bounds__(256)
     k_scatter_p2p(K keys, int64_t n, uint64_t seed, uint64_t nparts,
                   const double* __restrict__ entries, uint32_t bcount,
@@ -36,8 +37,12 @@ __global__ void __launch_bounds__(256)
     const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
     const uint32_t g = __ldg(owner + j);
     const uint32_t pos = atomicAdd(cursor + j, 1u);
-    peers.lo[g][pos] = h.lo;
-    peers.bid[g][pos] = (uint16_t)b;
+    if (REC) {  // one 16-byte peer store per key: {lo, bucket id}
+      reinterpret_cast<ulonglong2*>(peers.lo[g])[pos] = make_ulonglong2(h.lo, b);
+    } else {
+      peers.lo[g][pos] = h.lo;
+      peers.bid[g][pos] = (uint16_t)b;
+    }
   }
 }
 
@@ -70,19 +75,26 @@ int launch_scatter_p2p(const uint8_t* buf, const int64_t* offsets, const uint64_
                        uint32_t* cursor, cudaStream_t st) {
   if (G < 1 || G > 64 || nparts < 1) return 1003;
   PeerTable t;
-  for (int g = 0; g < G; ++g) t.lo[g] = lo_dst[g], t.bid[g] = bid_dst[g];
+  const bool rec = bid_dst == nullptr;  // 16-byte records in lo_dst
+  for (int g = 0; g < G; ++g) t.lo[g] = lo_dst[g], t.bid[g] = rec ? nullptr : bid_dst[g];
   note_launch(), k_cursor_from_i64<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
       part_base, nparts, cursor);
   PHB_CUDA_TRY(cudaGetLastError());
   if (n <= 0) return 0;
   int64_t need = (n + 255) / 256;
   int grid = (int)std::min<int64_t>(need, (int64_t)num_sms() * 16);
-  if (keys64)
-    note_launch(), k_scatter_p2p<<<grid, 256, 0, st>>>(U64KeysP{keys64}, n, seed, (uint64_t)nparts, entries,
-                                        bcount, owner, cursor, t);
+  if (keys64 && rec)
+    note_launch(), k_scatter_p2p<U64KeysP, true><<<grid, 256, 0, st>>>(
+        U64KeysP{keys64}, n, seed, (uint64_t)nparts, entries, bcount, owner, cursor, t);
+  else if (keys64)
+    note_launch(), k_scatter_p2p<U64KeysP, false><<<grid, 256, 0, st>>>(
+        U64KeysP{keys64}, n, seed, (uint64_t)nparts, entries, bcount, owner, cursor, t);
+  else if (rec)
+    note_launch(), k_scatter_p2p<ByteKeysP, true><<<grid, 256, 0, st>>>(
+        ByteKeysP{buf, offsets}, n, seed, (uint64_t)nparts, entries, bcount, owner, cursor, t);
   else
-    note_launch(), k_scatter_p2p<<<grid, 256, 0, st>>>(ByteKeysP{buf, offsets}, n, seed, (uint64_t)nparts,
-                                        entries, bcount, owner, cursor, t);
+    note_launch(), k_scatter_p2p<ByteKeysP, false><<<grid, 256, 0, st>>>(
+        ByteKeysP{buf, offsets}, n, seed, (uint64_t)nparts, entries, bcount, owner, cursor, t);
   return (int)cudaGetLastError();
 }
 

@@ -335,20 +335,21 @@ def build_distributed(local_keys, config: BuildConfig | None = None, group=None,
 
 
 class PeerBuffers:
-    """CUDA-IPC receive buffers of the fused p2p route, allocated once per
-    DeviceOps and kept mapped in every peer across builds; they grow
-    (collectively) only when some rank must receive more records than its
-    buffer holds. Every rank derives every rank's receive count from the
+    """CUDA-IPC receive buffers of the fused p2p route: one buffer of 16-byte
+    {lo, bucket id} records per rank (one peer store per key), allocated
+    once per DeviceOps and kept mapped in every peer across builds; they
+    grow (collectively) only when some rank must receive more records than
+    its buffer holds. Every rank derives every rank's receive count from the
     all-gathered per-partition counts, so the grow decision needs no extra
     collective."""
+
+    REC = 16  # bytes per record
 
     def __init__(self, group, rank: int, world: int):
         self.group, self.rank, self.world = group, rank, world
         self.caps = [0] * world          # records per rank (identical on every rank)
-        self.lo_p = ctypes.c_void_p()    # own receive buffers
-        self.bid_p = ctypes.c_void_p()
-        self.lo_ptrs = (ctypes.c_void_p * world)()
-        self.bid_ptrs = (ctypes.c_void_p * world)()
+        self.rec_p = ctypes.c_void_p()   # own receive buffer
+        self.rec_ptrs = (ctypes.c_void_p * world)()
         self.opened: list[int] = []      # mapped peer buffers (not ours)
         self.maps = 0                    # how many times the buffers were (re)mapped
 
@@ -358,11 +359,10 @@ class PeerBuffers:
         for ptr in self.opened:
             L.phb_ipc_close(ptr)
         self.opened = []
-        dist.barrier(group=self.group)  # every peer unmapped our buffers
-        if self.lo_p.value:
-            L.phb_ipc_free(self.lo_p)
-            L.phb_ipc_free(self.bid_p)
-        self.lo_p, self.bid_p = ctypes.c_void_p(), ctypes.c_void_p()
+        dist.barrier(group=self.group)  # every peer unmapped our buffer
+        if self.rec_p.value:
+            L.phb_ipc_free(self.rec_p)
+        self.rec_p = ctypes.c_void_p()
 
     def close(self) -> None:
         self._unmap()
@@ -371,19 +371,16 @@ class PeerBuffers:
     def ensure(self, recv: list[int], comm_dev) -> bool:
         """Make every rank's buffer hold recv[g] records (collective when
         any rank grows). False if some rank cannot map a peer buffer."""
-        if all(r <= c for r, c in zip(recv, self.caps)) and self.lo_p.value:
+        if all(r <= c for r, c in zip(recv, self.caps)) and self.rec_p.value:
             return True
         L = _native.lib()
         self._unmap()
         # 2% headroom so that the next builds (retries, other seeds) fit
         self.caps = [max(c, int(r * 1.02) + 4096) for r, c in zip(recv, self.caps)]
-        cap = self.caps[self.rank]
-        _native.check(L.phb_ipc_alloc(cap * 8, ctypes.byref(self.lo_p)), "phb_ipc_alloc")
-        _native.check(L.phb_ipc_alloc(cap * 2, ctypes.byref(self.bid_p)), "phb_ipc_alloc")
-        hbuf = np.zeros(128, np.uint8)
-        _native.check(L.phb_ipc_handle(self.lo_p, hbuf.ctypes.data_as(ctypes.c_void_p)),
-                      "phb_ipc_handle")
-        _native.check(L.phb_ipc_handle(self.bid_p, hbuf[64:].ctypes.data_as(ctypes.c_void_p)),
+        _native.check(L.phb_ipc_alloc(self.caps[self.rank] * self.REC, ctypes.byref(self.rec_p)),
+                      "phb_ipc_alloc")
+        hbuf = np.zeros(64, np.uint8)
+        _native.check(L.phb_ipc_handle(self.rec_p, hbuf.ctypes.data_as(ctypes.c_void_p)),
                       "phb_ipc_handle")
         mine = torch.from_numpy(hbuf).to(comm_dev)
         allh = [torch.empty_like(mine) for _ in range(self.world)]
@@ -391,19 +388,15 @@ class PeerBuffers:
         ok = True
         for g in range(self.world):
             if g == self.rank:
-                self.lo_ptrs[g], self.bid_ptrs[g] = self.lo_p.value, self.bid_p.value
+                self.rec_ptrs[g] = self.rec_p.value
                 continue
             h = np.ascontiguousarray(allh[g].cpu().numpy())
-            a, b = ctypes.c_void_p(), ctypes.c_void_p()
+            a = ctypes.c_void_p()
             if L.phb_ipc_open(h.ctypes.data_as(ctypes.c_void_p), ctypes.byref(a)) != 0:
                 ok = False
                 break
             self.opened.append(a.value)
-            if L.phb_ipc_open(h[64:].ctypes.data_as(ctypes.c_void_p), ctypes.byref(b)) != 0:
-                ok = False
-                break
-            self.opened.append(b.value)
-            self.lo_ptrs[g], self.bid_ptrs[g] = a.value, b.value
+            self.rec_ptrs[g] = a.value
         flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device=comm_dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
         self.maps += 1
@@ -468,12 +461,12 @@ def _route_p2p(ops: DeviceOps, dk: DeviceKeys, seed: int, nparts: int, C: torch.
     _native.check(L.phb_scatter_p2p(
         None if dk.is_u64 else P(dk.buf), None if dk.is_u64 else P(dk.offsets),
         P(dk.keys64) if dk.is_u64 else None, dk.n, seed, nparts, P(ops.entries), ops.B,
-        P(part_base), P(owner), pb.lo_ptrs, pb.bid_ptrs, world, P(cursor), _native.stream()),
+        P(part_base), P(owner), pb.rec_ptrs, None, world, P(cursor), _native.stream()),
         "phb_scatter_p2p")
     _fence(group, dev)  # every source finished writing into every owner
     key_off_own = (ex[p_lo:p_hi + 1] - ex[p_lo]).contiguous()
-    return (_PtrTensor(pb.lo_p.value, recv_n), _PtrTensor(pb.bid_p.value, recv_n), key_off_own,
-            None)
+    # 16-byte records: the search reads them with bid = NULL
+    return (_PtrTensor(pb.rec_p.value, 2 * recv_n), None, key_off_own, None)
 
 
 class _EngineView:
