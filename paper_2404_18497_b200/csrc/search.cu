@@ -467,7 +467,9 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     for (uint32_t i = 0; i < k; i += 2) {
       STAT(3, 2);
       const uint32_t pa = pp & 0xffffu, pb = pp >> 16;
-      pp = mp32[(i + 2 < k ? i + 2 : i) >> 1];
+      // the next pair's positions; past the last pair this reads a spare
+      // entry of the (256-entry) position area, never used
+      pp = mp32[(i >> 1) + 1];
       const uint32_t sa = pa & 31, sb = pb & 31;
       const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
       uint32_t xa = smem[Wa], xb = smem[Wb];
@@ -478,11 +480,8 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         xa = ya;
         xb = yb;
       }
-#ifdef PHB_CHECK2
-      if (i >= 2) {
-#else
-      if (i & 2u) {
-#endif
+      // every 4 keys, when keys remain: stop once every window is saturated
+      if ((i & 2u) && i + 2 < k) {
         uint32_t all = FULL;
 #pragma unroll
         for (int t = 0; t < WPL; ++t) all &= acc[t];
