@@ -295,16 +295,23 @@ __global__ void __launch_bounds__(1024, 1) k_hash_count_u64x4(const ulonglong2* 
   extern __shared__ uint32_t hist[];
   for (uint32_t t = threadIdx.x; t < nparts; t += blockDim.x) hist[t] = 0;
   __syncthreads();
-  const int64_t nq = n >> 2;
+#ifndef PHB_K1_NK
+#define PHB_K1_NK 8  // C2: 0.259 (4) -> 0.244 ms
+#endif
+  constexpr int NK = PHB_K1_NK;  // keys per thread per step (NK / 2 16-byte streaming loads)
+  const int64_t nq = n / NK;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const ulonglong2 a = __ldg(keys2 + 2 * q), c = __ldg(keys2 + 2 * q + 1);
-    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(a.x, seed).hi, nparts), 1u);
-    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(a.y, seed).hi, nparts), 1u);
-    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(c.x, seed).hi, nparts), 1u);
-    atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(c.y, seed).hi, nparts), 1u);
+    ulonglong2 v[NK / 2];
+#pragma unroll
+    for (int e = 0; e < NK / 2; ++e) v[e] = __ldcs(keys2 + (NK / 2) * q + e);
+#pragma unroll
+    for (int e = 0; e < NK / 2; ++e) {
+      atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(v[e].x, seed).hi, nparts), 1u);
+      atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(v[e].y, seed).hi, nparts), 1u);
+    }
   }
-  const int64_t t = (nq << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = nq * NK + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < n) {
     const uint64_t* keys = reinterpret_cast<const uint64_t*>(keys2);
     atomicAdd(hist + (uint32_t)mulhi(murmur3_u64(__ldg(keys + t), seed).hi, nparts), 1u);

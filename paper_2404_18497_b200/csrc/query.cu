@@ -155,28 +155,37 @@ __global__ void __launch_bounds__(256)
 // not two: the random gathers are what the L1 tag stage serialises (32
 // distinct lines per warp instruction). One 1024-thread CTA per SM, the
 // tables loaded once per CTA.
+#ifndef PHB_Q_NK
+#define PHB_Q_NK 4
+#endif
 __global__ void __launch_bounds__(1024, 1)
     k_query32s_u64x4(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
                      uint64_t nparts, const int64_t* __restrict__ key_off,
                      const double* __restrict__ entries, uint32_t bcount,
                      const uint32_t* __restrict__ seeds32, longlong2* __restrict__ out2) {
+  constexpr int NK = PHB_Q_NK;  // keys per thread per step
   extern __shared__ __align__(16) unsigned char q_smem[];
   double2* const tab = reinterpret_cast<double2*>(q_smem);
   uint32_t* const koff = reinterpret_cast<uint32_t*>(tab + BUCKET_TAB);
   for (int64_t j = threadIdx.x; j <= (int64_t)nparts; j += blockDim.x)
     koff[j] = (uint32_t)__ldg(key_off + j);
   load_bucket_pairs(entries, tab);  // ends with __syncthreads
-  const int64_t nv = nq >> 2;
+  const int64_t nv = nq / NK;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
        v += (int64_t)gridDim.x * blockDim.x) {
-    // streaming keys / outputs are marked evict-first so the seed table stays in L2
-    const ulonglong2 ka = __ldcs(keys2 + 2 * v), kc = __ldcs(keys2 + 2 * v + 1);
-    const uint64_t k[4] = {ka.x, ka.y, kc.x, kc.y};
-    uint64_t lo[4];
-    uint2 pe[4];
-    uint32_t p[4];
+    uint64_t k[NK];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < NK / 2; ++e) {
+      // streaming keys / outputs are marked evict-first so the seed table stays in L2
+      const ulonglong2 kv = __ldcs(keys2 + (NK / 2) * v + e);
+      k[2 * e] = kv.x;
+      k[2 * e + 1] = kv.y;
+    }
+    uint64_t lo[NK];
+    uint2 pe[NK];
+    uint32_t p[NK];
+#pragma unroll
+    for (int e = 0; e < NK; ++e) {
       const Hash128 h = murmur3_u64(k[e], seed);
       lo[e] = h.lo;
       const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
@@ -184,13 +193,13 @@ __global__ void __launch_bounds__(1024, 1)
       p[e] = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + j);
       pe[e] = make_uint2(koff[j], koff[j + 1]);
     }
-    int64_t r[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) r[e] = finish_query(lo[e], pe[e], n, p[e]);
-    __stcs(out2 + 2 * v, make_longlong2(r[0], r[1]));
-    __stcs(out2 + 2 * v + 1, make_longlong2(r[2], r[3]));
+    for (int e = 0; e < NK / 2; ++e)
+      __stcs(out2 + (NK / 2) * v + e, make_longlong2(finish_query(lo[2 * e], pe[2 * e], n, p[2 * e]),
+                                                     finish_query(lo[2 * e + 1], pe[2 * e + 1], n,
+                                                                  p[2 * e + 1])));
   }
-  const int64_t t = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t t = nv * NK + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < nq) {
     const Hash128 h = murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
     const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
