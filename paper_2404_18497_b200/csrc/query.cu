@@ -438,6 +438,88 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// K7es: K7e for large u64 batches of an interleaved structure, the K7s way:
+// partition offsets (u32), bucket pairs and the Compact columns' (payload bit,
+// width) in shared memory, four keys per thread, streaming keys / outputs.
+// A Compact query then makes one random access into the section (its field);
+// Rice columns take eget's select path (global descriptors).
+__global__ void __launch_bounds__(1024, 1)
+    k_query_enc_s(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
+                  uint64_t nparts, const int64_t* __restrict__ key_off,
+                  const double* __restrict__ entries, uint32_t bcount,
+                  const uint8_t* __restrict__ sec, const ECol* __restrict__ cols,
+                  const uint32_t* __restrict__ dsel, int64_t dstride,
+                  longlong2* __restrict__ out2) {
+  extern __shared__ __align__(16) unsigned char q_smem[];
+  double2* const tab = reinterpret_cast<double2*>(q_smem);
+  ulonglong2* const cdesc = reinterpret_cast<ulonglong2*>(tab + BUCKET_TAB);  // (pay bit, kind|width)
+  uint32_t* const koff = reinterpret_cast<uint32_t*>(cdesc + bcount);
+  for (uint32_t c = threadIdx.x; c < bcount; c += blockDim.x) {
+    const ECol d = cols[c];
+    cdesc[c] = make_ulonglong2(8ull * (uint64_t)d.pay_byte,
+                               ((uint64_t)(d.kind != 0) << 32) | (uint64_t)d.param);
+  }
+  for (int64_t j = threadIdx.x; j <= (int64_t)nparts; j += blockDim.x)
+    koff[j] = (uint32_t)__ldg(key_off + j);
+  load_bucket_pairs(entries, tab);  // ends with __syncthreads
+  const int64_t nv = nq >> 2;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 ka = __ldcs(keys2 + 2 * v), kc = __ldcs(keys2 + 2 * v + 1);
+    const uint64_t k[4] = {ka.x, ka.y, kc.x, kc.y};
+    int64_t r[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const Hash128 h = murmur3_u64(k[e], seed);
+      const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
+      const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
+      const int64_t offj = koff[j];
+      const int64_t m = (int64_t)koff[j + 1] - offj;
+      if (m <= 0) {
+        r[e] = offj < n ? offj : n - 1;
+        continue;
+      }
+      const ulonglong2 cd = cdesc[b - 1];
+      uint64_t p;
+      if ((cd.y >> 32) == 0) {  // CompactVector.get: one field
+        const int w = (int)(uint32_t)cd.y;
+        p = w ? ebits(sec, cd.x + (uint64_t)j * w, w) : 0ull;
+      } else {
+        p = eget(sec, cols + (b - 1), (int64_t)j, dsel ? dsel + (int64_t)(b - 1) * dstride : nullptr);
+      }
+      const uint64_t mu = (uint64_t)m;
+      const uint64_t sq = (p >> 32) ? p / mu : (uint64_t)((uint32_t)p / (uint32_t)mu);
+      const uint64_t d = p - sq * mu;
+      uint64_t pos = mulhi(mix64(h.lo ^ mix64(sq ^ POSITION_SALT)), mu) + d;
+      if (pos >= mu) pos -= mu;
+      r[e] = offj + (int64_t)pos;
+    }
+    __stcs(out2 + 2 * v, make_longlong2(r[0], r[1]));
+    __stcs(out2 + 2 * v + 1, make_longlong2(r[2], r[3]));
+  }
+  const int64_t t = (nv << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < nq) {
+    const Hash128 h = murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
+    const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
+    const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
+    const int64_t offj = koff[j];
+    const int64_t m = (int64_t)koff[j + 1] - offj;
+    int64_t rr;
+    if (m <= 0) {
+      rr = offj < n ? offj : n - 1;
+    } else {
+      const uint64_t p = eget(sec, cols + (b - 1), (int64_t)j,
+                              dsel ? dsel + (int64_t)(b - 1) * dstride : nullptr);
+      const uint64_t mu = (uint64_t)m;
+      const uint64_t sq = p / mu, d = p - sq * mu;
+      uint64_t pos = mulhi(mix64(h.lo ^ mix64(sq ^ POSITION_SALT)), mu) + d;
+      if (pos >= mu) pos -= mu;
+      rr = offj + (int64_t)pos;
+    }
+    reinterpret_cast<int64_t*>(out2)[t] = rr;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_verify(const int64_t* __restrict__ out, int64_t nq,
                                                 int64_t n, uint32_t* __restrict__ bitmap,
                                                 uint32_t* __restrict__ bad) {
@@ -537,7 +619,23 @@ int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint6
   if (nq <= 0) return 0;
   const int g = qgrid(nq);
   const ECol* c = reinterpret_cast<const ECol*>(cols);
-  if (keys64)
+  const size_t sh = sizeof(double2) * BUCKET_TAB + sizeof(ulonglong2) * bcount +
+                    sizeof(uint32_t) * (size_t)(nparts + 1);
+  int dev = 0, optin = 0;
+  PHB_CUDA_TRY(cudaGetDevice(&dev));
+  PHB_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  // large u64 batches of an interleaved section without a select directory
+  // (no Rice column: IC-C) take the shared-table kernel; Rice selects keep
+  // the many-CTA kernel, whose occupancy hides their scan latency better
+  if (keys64 && !mono && !dsel && n < ((int64_t)1 << 32) && sh <= (size_t)optin &&
+      nq >= (int64_t)num_sms() * 4096 && (reinterpret_cast<uintptr_t>(keys64) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    PHB_CUDA_TRY(cudaFuncSetAttribute(k_query_enc_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin));
+    note_launch(), k_query_enc_s<<<num_sms(), 1024, sh, st>>>(
+        reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, key_off,
+        entries, bcount, section, c, dsel, dstride, reinterpret_cast<longlong2*>(out));
+  } else if (keys64)
     note_launch(), k_query_enc<0><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
                                       entries, bcount, section, c, mono, dsel, dstride, out);
   else

@@ -105,3 +105,23 @@ def test_encoded_query_without_select_directory(phb):
                  _native.stream())
     assert torch.equal(out, with_dir)
     assert torch.equal(with_dir, f.query_device(dk))
+
+
+@pytest.mark.parametrize("enc", ["ic-c", "ic-r", "mixed:40"])
+def test_large_batch_encoded_query_shared_tables(phb, enc):
+    """Batches of >= 148 * 4096 u64 keys take the shared-memory matrix query
+    (K7s) and, for all-Compact sections, the shared-memory encoded query
+    (K7es: offsets, bucket pairs and column descriptors in shared memory);
+    every path equals the global-table kernels on a sample and is a
+    bijection."""
+    from paper_2404_18497_b200.keygen import DeviceKeys, synth_u64_device
+
+    n = 2_000_003  # odd: exercises the 4-key tail
+    keys = synth_u64_device(n, 99)
+    f = phb.build(DeviceKeys(n, keys64=keys),
+                  phb.BuildConfig(lambda_=7.0, partition_size=2500.0, encoder=enc))
+    big = f.query_encoded_device(DeviceKeys(n, keys64=keys))
+    assert f.verify_device(big)
+    assert torch.equal(big, f.query_device(DeviceKeys(n, keys64=keys)))
+    sample = keys[::101].contiguous()  # small batch: the global-table kernels
+    assert torch.equal(big[::101], f.query_encoded_device(DeviceKeys(sample.numel(), keys64=sample)))
