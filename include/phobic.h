@@ -94,6 +94,18 @@ int phb_bucket_ids(const uint64_t* his, int64_t n, const double* entries, int32_
 int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64, int64_t n,
                    uint64_t seed, int64_t nparts, uint32_t* counts, void* stream);
 
+/* K1 for byte keys that also keeps the 128-bit hashes: hashes_out[2i] = hi,
+ * hashes_out[2i+1] = lo (16-byte aligned, 2n u64), so K3 can run from them
+ * (phb_scatter_hashed) instead of hashing the key bytes again. */
+int phb_hash_count_store(const uint8_t* buf, const int64_t* offsets, int64_t n, uint64_t seed,
+                         int64_t nparts, uint32_t* counts, uint64_t* hashes_out, void* stream);
+
+/* K3 from stored hashes: the same 16-byte {lo, bucket id} records as
+ * phb_scatter with bid_out == NULL (rec_out: 2n u64). */
+int phb_scatter_hashed(const uint64_t* hashes, int64_t n, int64_t nparts, const double* entries,
+                       int32_t bcount, const int64_t* key_off, uint32_t* cursor, uint64_t* rec_out,
+                       void* stream);
+
 /* K2: counts[nparts] -> key_off[nparts+1] (local, from 0) and
  * deltas[nparts+1] = key_base + key_off[j] - expected(part_base + j,
  * global_n, global_nparts) (partitioning.py:101-108); stats[0] = max |delta|,

@@ -32,6 +32,8 @@ SIGNATURES = {
     "phb_bucket_ids": [P, I64, P, I32, P, P],
     "phb_hash_count": [P, P, P, I64, U64, I64, P, P],
     "phb_layout": [P, I64, I64, I64, I64, I64, P, P, P, P],
+    "phb_hash_count_store": [P, P, I64, U64, I64, P, P, P],
+    "phb_scatter_hashed": [P, I64, I64, P, I32, P, P, P, P],
     "phb_scatter": [P, P, P, I64, U64, I64, P, I32, P, P, P, P, P],
     "phb_scatter_padded": [P, I64, U64, I64, P, I32, I32, I32, P, P, P, P, P],
     "phb_padded_counts": [P, I64, I32, P, P, P],

@@ -134,6 +134,23 @@ int phb_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
   return launch_hash_count(buf, offsets, keys64, n, seed, (uint64_t)nparts, counts, S(stream));
 }
 
+int phb_hash_count_store(const uint8_t* buf, const int64_t* offsets, int64_t n, uint64_t seed,
+                         int64_t nparts, uint32_t* counts, uint64_t* hashes_out, void* stream) {
+  if (n < 0 || nparts < 1 || nparts >= (int64_t(1) << 32) || !hashes_out) return PHB_E_ARGS;
+  if (n > 0 && (!buf || !offsets)) return PHB_E_ARGS;
+  return launch_hash_count(buf, offsets, nullptr, n, seed, (uint64_t)nparts, counts, S(stream),
+                           hashes_out);
+}
+
+int phb_scatter_hashed(const uint64_t* hashes, int64_t n, int64_t nparts, const double* entries,
+                       int32_t bcount, const int64_t* key_off, uint32_t* cursor, uint64_t* rec_out,
+                       void* stream) {
+  if (bcount < 1 || bcount > 65535) return PHB_E_BUCKETS;
+  if (n < 0 || nparts < 1) return PHB_E_ARGS;
+  return launch_scatter_hashed(hashes, n, (uint64_t)nparts, entries, (uint32_t)bcount, key_off,
+                               cursor, rec_out, S(stream));
+}
+
 int phb_layout(uint32_t* counts, int64_t nparts, int64_t key_base, int64_t part_base,
                int64_t global_n, int64_t global_nparts, int64_t* key_off, int64_t* deltas,
                int64_t* stats, void* stream) {

@@ -50,10 +50,13 @@ __global__ void __launch_bounds__(256) k_murmur(K keys, int64_t n, uint64_t seed
 // K1: per-partition key counts. Small partition counts use a shared-memory
 // histogram per CTA (contention on few L2 lines otherwise); large ones go
 // straight to L2 atomics spread over nparts addresses.
+// store != NULL (byte keys): the 128-bit hashes are kept, (hi, lo) per key,
+// so that K3 (k_scatter_hashed) does not hash the key bytes a second time.
 template <class K, bool SMEM>
 __global__ void __launch_bounds__(256) k_hash_count(K keys, int64_t n, uint64_t seed,
                                                     uint64_t nparts,
-                                                    uint32_t* __restrict__ counts) {
+                                                    uint32_t* __restrict__ counts,
+                                                    ulonglong2* __restrict__ store) {
   extern __shared__ uint32_t sh_hist[];
   if (SMEM) {
     for (uint32_t t = threadIdx.x; t < nparts; t += blockDim.x) sh_hist[t] = 0;
@@ -62,6 +65,7 @@ __global__ void __launch_bounds__(256) k_hash_count(K keys, int64_t n, uint64_t 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     Hash128 h = keys.hash(i, seed);
+    if (store) store[i] = make_ulonglong2(h.hi, h.lo);
     uint32_t j = (uint32_t)mulhi(h.hi, nparts);
     if (SMEM)
       atomicAdd(sh_hist + j, 1u);
@@ -195,6 +199,39 @@ __global__ void __launch_bounds__(256) k_scatter_rec_u64(const ulonglong2* __res
     const Hash128 h = murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
     const uint32_t pos = atomicAdd(cursor + (uint32_t)mulhi(h.hi, nparts), 1u);
     rec_out[pos] = make_ulonglong2(h.lo, bucket_of_pairs(tab, h.hi, bcount));
+  }
+}
+
+// K3 from the hashes K1 stored (byte keys): (hi, lo) -> partition, bucket
+// id, 16-byte record at the partition's atomic cursor; 8 keys per thread.
+// The key bytes are hashed once per build instead of twice.
+__global__ void __launch_bounds__(256) k_scatter_hashed(const ulonglong2* __restrict__ hashes,
+                                                        int64_t n, uint64_t nparts,
+                                                        const double* __restrict__ entries,
+                                                        uint32_t bcount,
+                                                        uint32_t* __restrict__ cursor,
+                                                        ulonglong2* __restrict__ rec_out) {
+  constexpr int NK = 8;
+  __shared__ double2 tab[BUCKET_TAB];
+  load_bucket_pairs(entries, tab);
+  const int64_t nv = n / NK;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nv;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    ulonglong2 h[NK];
+#pragma unroll
+    for (int e = 0; e < NK; ++e) h[e] = __ldcs(hashes + NK * q + e);
+    uint32_t pos[NK];
+#pragma unroll
+    for (int e = 0; e < NK; ++e) pos[e] = atomicAdd(cursor + (uint32_t)mulhi(h[e].x, nparts), 1u);
+#pragma unroll
+    for (int e = 0; e < NK; ++e)
+      rec_out[pos[e]] = make_ulonglong2(h[e].y, bucket_of_pairs(tab, h[e].x, bcount));
+  }
+  const int64_t t = nv * NK + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) {
+    const ulonglong2 hh = __ldg(hashes + t);
+    const uint32_t pos = atomicAdd(cursor + (uint32_t)mulhi(hh.x, nparts), 1u);
+    rec_out[pos] = make_ulonglong2(hh.y, bucket_of_pairs(tab, hh.x, bcount));
   }
 }
 
@@ -360,9 +397,11 @@ static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t
 
 int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                       int64_t n, uint64_t seed, uint64_t nparts, uint32_t* counts,
-                      cudaStream_t st) {
+                      cudaStream_t st, uint64_t* hashes_out) {
   if (n <= 0) return 0;
   int g = grid_for(n);
+  ulonglong2* const store = reinterpret_cast<ulonglong2*>(hashes_out);
+  if (keys64 && store) return 1003;  // u64 keys re-hash cheaply; the store is for byte keys
   if (keys64 && aligned16(keys64) && nparts > SMEM_HIST_MAX && nparts <= SMEM_HIST_MAX_BIG) {
     size_t sh = nparts * sizeof(uint32_t);
     // the largest histogram this path takes (not this launch's size): a
@@ -381,16 +420,16 @@ int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t
     int gs = g < 2 * num_sms() ? g : 2 * num_sms();
     size_t sh = nparts * sizeof(uint32_t);
     if (keys64)
-      note_launch(), k_hash_count<U64Keys, true><<<gs, 256, sh, st>>>(U64Keys{keys64}, n, seed, nparts, counts);
+      note_launch(), k_hash_count<U64Keys, true><<<gs, 256, sh, st>>>(U64Keys{keys64}, n, seed, nparts, counts, nullptr);
     else
       note_launch(), k_hash_count<ByteKeys, true>
-          <<<gs, 256, sh, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, counts);
+          <<<gs, 256, sh, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, counts, store);
   } else {
     if (keys64)
-      note_launch(), k_hash_count<U64Keys, false><<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, counts);
+      note_launch(), k_hash_count<U64Keys, false><<<g, 256, 0, st>>>(U64Keys{keys64}, n, seed, nparts, counts, nullptr);
     else
       note_launch(), k_hash_count<ByteKeys, false>
-          <<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, counts);
+          <<<g, 256, 0, st>>>(ByteKeys{buf, offsets}, n, seed, nparts, counts, store);
   }
   return (int)cudaGetLastError();
 }
@@ -456,6 +495,21 @@ int launch_bucket_ids(const uint64_t* his, int64_t n, const double* entries, uin
                       uint16_t* bid, cudaStream_t st) {
   if (n <= 0) return 0;
   note_launch(), k_bucket_ids<<<grid_for(n), 256, 0, st>>>(his, n, entries, bcount, bid);
+  return (int)cudaGetLastError();
+}
+
+int launch_scatter_hashed(const uint64_t* hashes, int64_t n, uint64_t nparts,
+                          const double* entries, uint32_t bcount, const int64_t* key_off,
+                          uint32_t* cursor, uint64_t* rec_out, cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (n >= (int64_t(1) << 32)) return 1003;  // u32 cursors
+  if (reinterpret_cast<uintptr_t>(hashes) & 15) return 1003;
+  note_launch(), k_cursor_init<<<(int)std::min<int64_t>((nparts + 255) / 256, 4096), 256, 0, st>>>(
+      key_off, (int64_t)nparts, cursor);
+  PHB_CUDA_TRY(cudaGetLastError());
+  note_launch(), k_scatter_hashed<<<grid_for((n + 7) / 8), 256, 0, st>>>(
+      reinterpret_cast<const ulonglong2*>(hashes), n, nparts, entries, bcount, cursor,
+      reinterpret_cast<ulonglong2*>(rec_out));
   return (int)cudaGetLastError();
 }
 

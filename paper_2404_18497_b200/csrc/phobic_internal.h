@@ -22,7 +22,10 @@ int launch_murmur(const uint8_t* buf, const int64_t* offsets, const uint64_t* ke
                   uint64_t seed, uint64_t* hi, uint64_t* lo, cudaStream_t st);
 int launch_hash_count(const uint8_t* buf, const int64_t* offsets, const uint64_t* keys64,
                       int64_t n, uint64_t seed, uint64_t nparts, uint32_t* counts,
-                      cudaStream_t st);
+                      cudaStream_t st, uint64_t* hashes_out = nullptr);
+int launch_scatter_hashed(const uint64_t* hashes, int64_t n, uint64_t nparts,
+                          const double* entries, uint32_t bcount, const int64_t* key_off,
+                          uint32_t* cursor, uint64_t* rec_out, cudaStream_t st);
 int launch_scatter_padded(const uint64_t* keys64, int64_t n, uint64_t seed, uint64_t nparts,
                           const double* entries, uint32_t bcount, uint32_t cap, int init,
                           uint32_t* cursor, uint64_t* lo_out, uint16_t* bid_out,

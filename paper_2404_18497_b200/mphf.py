@@ -214,8 +214,15 @@ class BuildEngine:
                                 part_trials)
 
         counts = torch.zeros(nparts, dtype=torch.int32, device=dev)
-        _native.check(L.phb_hash_count(buf, offs, k64, n, seed, nparts, P(counts), st),
-                      "phb_hash_count")
+        # byte keys: K1 keeps the 128-bit hashes so K3 does not hash the bytes again
+        hashes = None
+        if not dk.is_u64 and not instrument:
+            hashes = torch.empty(2 * n, dtype=torch.int64, device=dev)
+            _native.check(L.phb_hash_count_store(buf, offs, n, seed, nparts, P(counts), P(hashes),
+                                                 st), "phb_hash_count_store")
+        else:
+            _native.check(L.phb_hash_count(buf, offs, k64, n, seed, nparts, P(counts), st),
+                          "phb_hash_count")
         key_off = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
         deltas = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
         stats = torch.empty(2, dtype=torch.int64, device=dev)
@@ -233,8 +240,14 @@ class BuildEngine:
         else:
             lo = torch.empty(2 * n, dtype=torch.int64, device=dev)
             bid = None
-        _native.check(L.phb_scatter(buf, offs, k64, n, seed, nparts, P(self.entries), B,
-                                    P(key_off), P(counts), P(lo), P(bid), st), "phb_scatter")
+        if hashes is not None:
+            _native.check(L.phb_scatter_hashed(P(hashes), n, nparts, P(self.entries), B,
+                                               P(key_off), P(counts), P(lo), st),
+                          "phb_scatter_hashed")
+            del hashes
+        else:
+            _native.check(L.phb_scatter(buf, offs, k64, n, seed, nparts, P(self.entries), B,
+                                        P(key_off), P(counts), P(lo), P(bid), st), "phb_scatter")
         seeds = torch.zeros(B * nparts, dtype=torch.int64, device=dev)
         trials = torch.zeros(B * nparts, dtype=torch.int64, device=dev) if instrument else None
         sizes = None

@@ -21,7 +21,7 @@ dk = DeviceKeys(n, buf=buf, offsets=offsets)
 eng = BuildEngine(phb.BuildConfig(lambda_=8.0, partition_size=2500.0, encoder="ic-r"))
 L = _native.lib()
 times = {}
-for name in ["phb_hash_count", "phb_layout", "phb_scatter", "phb_search", "phb_encode_plan",
+for name in ["phb_hash_count", "phb_hash_count_store", "phb_layout", "phb_scatter", "phb_scatter_hashed", "phb_search", "phb_encode_plan",
              "phb_encode_write"]:
     fn = getattr(L, name)
 
@@ -43,5 +43,5 @@ for r in range(3):
     parts = {k: sum(a.elapsed_time(b) for a, b in v) for k, v in times.items()}
     print(f"rep {r}: " + "  ".join(f"{k[4:]}={v:.3f}ms" for k, v in parts.items()), flush=True)
 bytes_per_pass = total + 8 * (n + 1)
-print(f"key bytes {total / n:.1f} B/key; hash_count {bytes_per_pass / parts['phb_hash_count'] / 1e6:.0f} GB/s,"
-      f" scatter read {bytes_per_pass / parts['phb_scatter'] / 1e6:.0f} GB/s")
+print(f"key bytes {total / n:.1f} B/key; hash_count {bytes_per_pass / parts.get('phb_hash_count', parts.get('phb_hash_count_store')) / 1e6:.0f} GB/s,"
+      f" scatter read {bytes_per_pass / parts.get('phb_scatter', parts.get('phb_scatter_hashed')) / 1e6:.0f} GB/s")
