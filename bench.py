@@ -370,18 +370,27 @@ def _config_row(name, dk, cfg, reps, extra=None):
 
     eng = BuildEngine(cfg)
     res = eng.run(dk, 0)  # warm-up
-    ms, res = _timed(lambda: eng.run(dk, 0), reps)
+    times = []
+    for _ in range(reps):  # per-build device times; the median is reported
+        t, res = _timed(lambda: eng.run(dk, 0), 1)
+        times.append(t)
+    ms = statistics.median(times)
     assert not isinstance(res, tuple), f"{name}: build failed"
     f = phb.Mphf._from_device(res, cfg, eng, None)
     out = f.query_device(dk)
     ok = f.verify_device(out)
     q_ms, _ = _timed(lambda: f.query_device(dk), 3)
     n = dk.n
+    fut = getattr(f, "_ck_future", None)
+    if fut is not None:
+        fut.result()  # the host-side checksum thread is idle before the next row times
     row = {"config": name, "n": n, "lambda": cfg.lambda_, "encoder": cfg.encoder,
-           "build_ms": round(ms, 3), "ns_per_key": ms * 1e6 / n, "keys_per_s": n / (ms * 1e-3),
+           "build_ms": round(ms, 3), "build_ms_reps": [round(t, 3) for t in times],
+           "ns_per_key": ms * 1e6 / n, "keys_per_s": n / (ms * 1e-3),
            "bits_per_key": (res.total_bytes + 8 - 16) * 8 / n,
            "trials_per_key": res.trials_total / n, "query_ms": round(q_ms, 3),
-           "query_Mq_s": n / (q_ms * 1e-3) / 1e6, "bijection": bool(ok), "reps": reps}
+           "query_Mq_s": n / (q_ms * 1e-3) / 1e6, "bijection": bool(ok), "reps": reps,
+           "timing": "median of per-build CUDA-event times"}
     if extra:
         row.update(extra)
     del f, res, eng, out
@@ -405,18 +414,18 @@ def run_configs(dev, args):
     dk = DeviceKeys(args.n, keys64=keys)
     for lam in (4.0, 5.0, 6.0, 7.0, 8.0, 9.0):
         rows.append(_config_row(f"C4: {args.n / 1e6:g}M u64, lambda={lam:g}, IC-R", dk,
-                                cfg(lam, "ic-r"), 3))
+                                cfg(lam, "ic-r"), 5))
     del keys, dk
     torch.cuda.empty_cache()
     dk, total = _string_keys(args.n, 10, 100, 2024, dev)
     rows.append(_config_row(f"C5: {args.n / 1e6:g}M strings of 10-100 B, lambda=8, IC-R", dk,
-                            cfg(8.0, "ic-r"), 3,
+                            cfg(8.0, "ic-r"), 5,
                             {"mean_key_bytes": total / args.n, "key_bytes_total": total}))
     del dk
     torch.cuda.empty_cache()
     dk, total = _string_keys(args.n, 10, 50, 2025, dev)
     paper = _config_row(f"paper: {args.n / 1e6:g}M strings of 10-50 B, lambda=9, IC-C", dk,
-                        cfg(9.0, "ic-c"), 3,
+                        cfg(9.0, "ic-c"), 5,
                         {"mean_key_bytes": total / args.n, "key_bytes_total": total,
                          "published_ns_per_key": PUBLISHED_NS_PER_KEY,
                          "published": "PHOBIC-GPU, RTX 3090 + 8 CPU threads, 2.17 bits/key "
