@@ -406,27 +406,10 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     const int64_t s = s_next + grp;
     const uint64_t g = seed_hash(s);
     const uint32_t p = position(key, g, m);
-#ifdef PHB_SHFL_COLL
-    // self-collision inside the lane group by butterfly shuffles (G > 1:
-    // L - 1 rounds, no MATCH.ANY latency on the critical path)
-    bool mycoll = false;
-    if constexpr (G > 1) {
-      const uint32_t pv = act ? p : (0x80000000u | (uint32_t)lane);
-#pragma unroll
-      for (int o = 1; o < L; ++o) mycoll |= __shfl_xor_sync(FULL, pv, o) == pv;
-      mycoll = mycoll && act;
-    } else {
-      const uint32_t tag = act ? p : (0x80000000u | (uint32_t)lane);
-      const uint32_t peers = __match_any_sync(FULL, tag);  // every lane votes
-      mycoll = act && __popc(peers) > 1;
-    }
-    const uint32_t cball = __ballot_sync(FULL, mycoll);
-#else
     const uint32_t tag = act ? (((uint32_t)grp << 16) | p) : (0x80000000u | (uint32_t)lane);
     // every lane must execute the vote (no short-circuit around it)
     const uint32_t tpeers = __match_any_sync(FULL, tag);
     const uint32_t cball = __ballot_sync(FULL, act && __popc(tpeers) > 1);
-#endif
     if (act) mypos[gl] = (uint16_t)p;
 #ifndef PHB_NOPAIR
     // keys are swept in pairs: an odd k repeats its last key (OR is idempotent)
