@@ -163,8 +163,11 @@ __global__ void __launch_bounds__(256) k_scatter_u64x4(const ulonglong2* __restr
 // Record-layout u64 scatter with NK keys per thread per step (NK / 2 16-byte
 // loads): NK independent hash -> cursor atomic -> record store chains in
 // flight per thread (the atomics' L2 round trips are the latency to hide).
+#ifndef PHB_K3_MINB
+#define PHB_K3_MINB 1
+#endif
 template <int NK>
-__global__ void __launch_bounds__(256) k_scatter_rec_u64(const ulonglong2* __restrict__ keys2,
+__global__ void __launch_bounds__(256, PHB_K3_MINB) k_scatter_rec_u64(const ulonglong2* __restrict__ keys2,
                                                          int64_t n, uint64_t seed, uint64_t nparts,
                                                          const double* __restrict__ entries,
                                                          uint32_t bcount,
