@@ -153,3 +153,25 @@ def test_c3_billion_keys_sampled_partitions_vs_oracle(phb, orc):
     assert not status.any()
     assert np.array_equal(seeds, seeds_dev.view(np.uint64))
     assert np.array_equal(trials, trials_dev)
+
+
+@pytest.mark.parametrize("lam", [4.0, 5.0])
+def test_c4_low_lambda_full_size_vs_oracle(phb, orc, lam):
+    """C4's low-lambda end at full size (100M u64 keys, IC-R): the low-lambda
+    search kernel (speculative seed-0 steps over four buckets, batched
+    singletons) gives the oracle's bytes and trial total."""
+    from paper_2404_18497_b200.keygen import DeviceKeys, synth_u64, synth_u64_device
+    from paper_2404_18497_b200.mphf import HEADER_FIXED, BuildEngine
+
+    n = 100_000_000
+    cfg = phb.BuildConfig(lambda_=lam, partition_size=2500.0, encoder="ic-r")
+    dkeys = synth_u64_device(n, 7)
+    db = BuildEngine(cfg).run(DeviceKeys(n, keys64=dkeys), 0)
+    body = db.blob[HEADER_FIXED:db.total_bytes].cpu().numpy()
+    trials = db.trials_total
+    del db, dkeys
+    torch.cuda.empty_cache()
+    ref = orc.build(synth_u64(n, 7), lambda_=lam, P=2500.0, encoder="ic-r", threads=THREADS)
+    rblob = np.frombuffer(ref.serialize(), np.uint8)
+    assert np.array_equal(rblob[HEADER_FIXED:len(rblob) - 8], body)
+    assert trials == int(ref.trials.sum())
