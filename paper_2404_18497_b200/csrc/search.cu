@@ -90,6 +90,8 @@ __host__ __device__ inline SmemPlan smem_plan(int64_t m_max, uint32_t bcount) {
   // the bucket-order scratch (shist/srun) is dead before the search state
   // (mask table, collision map, positions) is written: they share one region
   const int search_w = 96 + p.scr_w + p.pos_w;
+  // the mask table (first word of the search union) 16-byte aligned for vector loads
+  p.ord_w = ((p.occ_w + 2 * p.cnt_w + p.ord_w + 3) & ~3) - p.occ_w - 2 * p.cnt_w;
   p.total_w = p.occ_w + 2 * p.cnt_w + p.ord_w + (p.sh_w > search_w ? p.sh_w : search_w);
   p.total_w = (p.total_w + 3) & ~3;  // 16-byte aligned warp regions (LDS.128)
   return p;
@@ -259,6 +261,50 @@ __device__ int64_t find_d(uint32_t occ, const uint16_t* pos16, uint32_t k,
 }
 
 
+// find_d for buckets of k >= 2 keys, keys swept in pairs: both windows are
+// OR-ed into the accumulators with one 3-input LOP3 per word (as in
+// small_bucket); an odd k repeats its last key (OR is idempotent).
+__device__ int64_t find_d_pairs(uint32_t occ, const uint16_t* pos16, uint32_t k, int64_t dmax,
+                                const uint64_t* kl, uint64_t g, uint32_t m, int lane) {
+  const uint32_t nwd = (uint32_t)((dmax + 32) >> 5);
+#pragma unroll 1
+  for (uint32_t g0 = 0; g0 < nwd; g0 += 96) {
+    const uint32_t wb = g0 + 3u * lane;
+    uint32_t a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll 1
+    for (uint32_t i = 0; i < k; i += 2) {
+      const uint32_t i2 = i + 1 < k ? i + 1 : i;
+      const uint32_t pa = k <= (uint32_t)PMAX ? (uint32_t)pos16[i] : position(kl[i], g, m);
+      const uint32_t pb = k <= (uint32_t)PMAX ? (uint32_t)pos16[i2] : position(kl[i2], g, m);
+      const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
+      const uint32_t sa = pa & 31, sb = pb & 31;
+      const uint32_t x0 = smem[Wa], x1 = smem[Wa + 1], x2 = smem[Wa + 2], x3 = smem[Wa + 3];
+      const uint32_t y0 = smem[Wb], y1 = smem[Wb + 1], y2 = smem[Wb + 2], y3 = smem[Wb + 3];
+      a0 |= __funnelshift_r(x0, x1, sa) | __funnelshift_r(y0, y1, sb);
+      a1 |= __funnelshift_r(x1, x2, sa) | __funnelshift_r(y1, y2, sb);
+      a2 |= __funnelshift_r(x2, x3, sa) | __funnelshift_r(y2, y3, sb);
+      if ((i & 2u) && i + 2 < k && __all_sync(FULL, (a0 & a1 & a2) == FULL)) break;
+    }
+    uint32_t v0 = ~a0, v1 = ~a1, v2 = ~a2;
+    const int64_t lim = dmax - 32 * (int64_t)wb;
+    if (lim < 95) {
+      v0 = lim < 0 ? 0u : (lim < 31 ? v0 & ((2u << lim) - 1u) : v0);
+      v1 = lim < 32 ? 0u : (lim < 63 ? v1 & ((2u << (lim - 32)) - 1u) : v1);
+      v2 = lim < 64 ? 0u : (lim < 95 ? v2 & ((2u << (lim - 64)) - 1u) : v2);
+    }
+    const uint32_t bal = __ballot_sync(FULL, (v0 | v1 | v2) != 0);
+    if (bal) {
+      const int l = __ffs(bal) - 1;
+      const uint32_t t = v0 ? 0u : (v1 ? 1u : 2u);
+      const uint32_t vv = v0 ? v0 : (v1 ? v1 : v2);
+      const uint32_t word = __shfl_sync(FULL, t, l);
+      const uint32_t bits = __shfl_sync(FULL, vv, l);
+      return 32 * (int64_t)(g0 + 3u * l + word) + (__ffs(bits) - 1);
+    }
+  }
+  return -1;
+}
+
 // Outcome of one bucket's search.
 struct BucketResult {
   int64_t seed, trials;
@@ -354,7 +400,7 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
     }
     int64_t dmax = cap - pbase;
     if (dmax > (int64_t)m - 1) dmax = (int64_t)m - 1;
-    const int64_t d = find_d(occ, pos16, k, dmax, kl, g, m, lane);
+    const int64_t d = find_d_pairs(occ, pos16, k, dmax, kl, g, m, lane);
     if (d >= 0) {
       trials += (int64_t)k * (d + 1);
 #pragma unroll 1
@@ -426,8 +472,25 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     uint32_t acc[WPL];
     if (G > 1) {
       // a self-colliding group (rare) is masked out after the sweep instead
+      // vector loads of the mask table (3 LDS.128 instead of 12 LDS at G = 4)
+      if constexpr (WPL % 4 == 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(smem + dmask + wb);
 #pragma unroll
-      for (int t = 0; t < WPL; ++t) acc[t] = smem[dmask + wb + t];
+        for (int t = 0; t < WPL / 4; ++t) {
+          const uint4 v = src[t];
+          acc[4 * t] = v.x, acc[4 * t + 1] = v.y, acc[4 * t + 2] = v.z, acc[4 * t + 3] = v.w;
+        }
+      } else if constexpr (WPL % 2 == 0) {
+        const uint2* src = reinterpret_cast<const uint2*>(smem + dmask + wb);
+#pragma unroll
+        for (int t = 0; t < WPL / 2; ++t) {
+          const uint2 v = src[t];
+          acc[2 * t] = v.x, acc[2 * t + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < WPL; ++t) acc[t] = smem[dmask + wb + t];
+      }
     } else if (dmax == (int64_t)m - 1) {
 #pragma unroll
       for (int t = 0; t < WPL; ++t) acc[t] = dead_group ? FULL : smem[dmask + wb + t];
@@ -464,7 +527,9 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         xb = yb;
       }
       // every 4 keys, when keys remain: stop once every window is saturated
-      if ((i & 2u) && i + 2 < k) {
+      // (not at G = 4: k <= 8 buckets almost never saturate all four groups
+      // before their last pair, so the check only costs issue slots)
+      if (G < 4 && (i & 2u) && i + 2 < k) {
         uint32_t all = FULL;
 #pragma unroll
         for (int t = 0; t < WPL; ++t) all &= acc[t];
@@ -521,10 +586,11 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
       const int src = __ffs(fball) - 1;  // first lane with a valid d lies in the first found group
       const int gw = src < 0 ? G : src / L;
       const int ncoll = __popc(collg & ((1u << gw) - 1u));
-      trials += (int64_t)k * ncoll + (int64_t)k * m * (gw - ncoll);
+      // k <= 16, m <= 3072, gw <= 4: every term fits 32 bits
+      const uint32_t tr = k * ((uint32_t)ncoll + m * (uint32_t)(gw - ncoll));
       if (src >= 0) {
-        const int64_t d = __shfl_sync(FULL, myd, src);
-        trials += (int64_t)k * (d + 1);
+        const uint32_t d = __shfl_sync(FULL, myd, src);
+        trials += (int64_t)(tr + k * (d + 1u));
         if (grp == gw && act) {
           uint32_t slot = p + (uint32_t)d;
           if (slot >= m) slot -= m;
@@ -532,6 +598,7 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         }
         return {(s_next + gw) * (int64_t)m + d, trials, 0};
       }
+      trials += (int64_t)tr;
       s_next += G;
       __syncwarp();
     } else {
