@@ -67,6 +67,15 @@ __device__ __forceinline__ uint64_t seed_hash(int64_t s) {
   return s < GTAB_N ? __ldg(&g_seed_hash.v[s]) : mix64((uint64_t)s ^ POSITION_SALT);
 }
 
+// window words of the batched seed steps (multiples of 8 / 16 lanes; a
+// partition takes the G = 4 / G = 2 step only if its m bits fit the window)
+#ifndef PHB_W4
+#define PHB_W4 88  // C2 search 23.26 -> 23.00 ms (m_max ~2,700 < 2,816 bits)
+#endif
+#ifndef PHB_W2
+#define PHB_W2 96
+#endif
+constexpr int W4 = PHB_W4, W2 = PHB_W2;
 constexpr int SH = 256;     // size classes of the counting-sort bucket order
 constexpr int PMAX = 256;   // bucket sizes whose base positions are staged in smem
 constexpr int WARPS = 4;    // warps (= partitions in flight) per CTA
@@ -429,12 +438,13 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
 // generic resolution); anything else is left to G = 1 steps. Returns
 // status -1 when max_batches ran out (or the batch would need the generic
 // resolution) without a decision; the caller continues.
-template <int G>
+template <int G, int W = 96>
 __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos16, uint32_t k,
                                      const uint64_t* kl, uint32_t m, int64_t cap,
                                      int64_t& s_next, int64_t trials, int max_batches,
                                      int lane) {
-  constexpr int L = 32 / G, WPL = 96 / L;
+  constexpr int L = 32 / G, WPL = W / L;  // W: window words per seed (W >= (m + 31) / 32)
+  static_assert(W % L == 0 && W <= 96, "window");
   constexpr uint32_t LMASK = L == 32 ? FULL : ((1u << L) - 1u);
   const int grp = lane / L, gl = lane % L;
   const bool act = (uint32_t)gl < k;
@@ -963,10 +973,12 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
                               lane);
         if (res.status < 0) {
           // batched instantiations hold 32 / G lanes per seed: only k <= 16
-          if (k <= 8)
-            res = small_bucket<4>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
-          else if (k <= kg1)
-            res = small_bucket<2>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30, lane);
+          if (k <= 8 && (W4 >= 96 || m <= 32u * W4))
+            res = small_bucket<4, W4>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
+                                      lane);
+          else if (k <= kg1 && (W2 >= 96 || m <= 32u * W2))
+            res = small_bucket<2, W2>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
+                                      lane);
           // near the seed cap, or k > 16: single-seed steps until decided
           while (res.status < 0)
             res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
