@@ -158,6 +158,11 @@ __global__ void __launch_bounds__(256)
 #ifndef PHB_Q_NK
 #define PHB_Q_NK 4
 #endif
+// Seed hashes mix64(s ^ POSITION_SALT) of seeds s < QGT_N, for the
+// encoded-section kernel's shared table (K7es); the matrix kernel K7s keeps
+// the 64-bit mix (a table there measured 3% slower).
+constexpr int QGT_N = 256;
+
 __global__ void __launch_bounds__(1024, 1)
     k_query32s_u64x4(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
                      uint64_t nparts, const int64_t* __restrict__ key_off,
@@ -443,6 +448,11 @@ __global__ void __launch_bounds__(256)
 // width) in shared memory, four keys per thread, streaming keys / outputs.
 // A Compact query then makes one random access into the section (its field);
 // Rice columns take eget's select path (global descriptors).
+// C32 (sections below 4 GB): the column descriptors as 8-byte (payload byte,
+// kind | width) pairs and the seed hashes of seeds < QGT_N in shared memory,
+// which keeps the C2 footprint under the 196 KB carveout step (16-byte
+// descriptors put it at 197.6 KB -> 228 KB carveout, L1 60 -> 28 KB).
+template <bool C32>
 __global__ void __launch_bounds__(1024, 1)
     k_query_enc_s(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
                   uint64_t nparts, const int64_t* __restrict__ key_off,
@@ -453,12 +463,21 @@ __global__ void __launch_bounds__(1024, 1)
   extern __shared__ __align__(16) unsigned char q_smem[];
   double2* const tab = reinterpret_cast<double2*>(q_smem);
   ulonglong2* const cdesc = reinterpret_cast<ulonglong2*>(tab + BUCKET_TAB);  // (pay bit, kind|width)
-  uint32_t* const koff = reinterpret_cast<uint32_t*>(cdesc + bcount);
+  uint2* const cdesc32 = reinterpret_cast<uint2*>(tab + BUCKET_TAB);          // (pay byte, kind<<31|width)
+  uint64_t* const gt = C32 ? reinterpret_cast<uint64_t*>(cdesc32 + ((bcount + 1) & ~1u)) : nullptr;
+  uint32_t* const koff = C32 ? reinterpret_cast<uint32_t*>(gt + QGT_N)
+                             : reinterpret_cast<uint32_t*>(cdesc + bcount);
   for (uint32_t c = threadIdx.x; c < bcount; c += blockDim.x) {
     const ECol d = cols[c];
-    cdesc[c] = make_ulonglong2(8ull * (uint64_t)d.pay_byte,
-                               ((uint64_t)(d.kind != 0) << 32) | (uint64_t)d.param);
+    if (C32)
+      cdesc32[c] = make_uint2((uint32_t)d.pay_byte,
+                              ((uint32_t)(d.kind != 0) << 31) | (uint32_t)d.param);
+    else
+      cdesc[c] = make_ulonglong2(8ull * (uint64_t)d.pay_byte,
+                                 ((uint64_t)(d.kind != 0) << 32) | (uint64_t)d.param);
   }
+  if (C32)
+    for (int t = threadIdx.x; t < QGT_N; t += blockDim.x) gt[t] = mix64((uint64_t)t ^ POSITION_SALT);
   for (int64_t j = threadIdx.x; j <= (int64_t)nparts; j += blockDim.x)
     koff[j] = (uint32_t)__ldg(key_off + j);
   load_bucket_pairs(entries, tab);  // ends with __syncthreads
@@ -479,18 +498,28 @@ __global__ void __launch_bounds__(1024, 1)
         r[e] = offj < n ? offj : n - 1;
         continue;
       }
-      const ulonglong2 cd = cdesc[b - 1];
+      uint64_t pbit, kw;
+      if (C32) {
+        const uint2 cd = cdesc32[b - 1];
+        pbit = 8ull * cd.x;
+        kw = cd.y;
+      } else {
+        const ulonglong2 cd = cdesc[b - 1];
+        pbit = cd.x;
+        kw = (cd.y >> 32) ? (1u << 31) | (uint32_t)cd.y : (uint32_t)cd.y;
+      }
       uint64_t p;
-      if ((cd.y >> 32) == 0) {  // CompactVector.get: one field
-        const int w = (int)(uint32_t)cd.y;
-        p = w ? ebits(sec, cd.x + (uint64_t)j * w, w) : 0ull;
+      if ((kw >> 31) == 0) {  // CompactVector.get: one field
+        const int w = (int)(kw & 0x7fffffffu);
+        p = w ? ebits(sec, pbit + (uint64_t)j * w, w) : 0ull;
       } else {
         p = eget(sec, cols + (b - 1), (int64_t)j, dsel ? dsel + (int64_t)(b - 1) * dstride : nullptr);
       }
       const uint64_t mu = (uint64_t)m;
       const uint64_t sq = (p >> 32) ? p / mu : (uint64_t)((uint32_t)p / (uint32_t)mu);
       const uint64_t d = p - sq * mu;
-      uint64_t pos = mulhi(mix64(h.lo ^ mix64(sq ^ POSITION_SALT)), mu) + d;
+      const uint64_t g = C32 && sq < (uint64_t)QGT_N ? gt[sq] : mix64(sq ^ POSITION_SALT);
+      uint64_t pos = mulhi(mix64(h.lo ^ g), mu) + d;
       if (pos >= mu) pos -= mu;
       r[e] = offj + (int64_t)pos;
     }
@@ -621,20 +650,37 @@ int launch_query_encoded(const uint8_t* buf, const int64_t* offsets, const uint6
   const ECol* c = reinterpret_cast<const ECol*>(cols);
   const size_t sh = sizeof(double2) * BUCKET_TAB + sizeof(ulonglong2) * bcount +
                     sizeof(uint32_t) * (size_t)(nparts + 1);
+  // compact descriptors: payload byte offsets below 2^32 (n < 2^29 keys bounds
+  // the section by 8 bytes per seed entry, i.e. below 4 GB)
+  const size_t sh32 = sizeof(double2) * BUCKET_TAB + sizeof(uint2) * ((bcount + 1) & ~1u) +
+                      sizeof(uint64_t) * QGT_N + sizeof(uint32_t) * (size_t)(nparts + 1);
   int dev = 0, optin = 0;
   PHB_CUDA_TRY(cudaGetDevice(&dev));
   PHB_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+#ifdef PHB_NO_C32
+  const bool c32 = false;
+#else
+  const bool c32 = n < ((int64_t)1 << 29) && sh32 <= (size_t)optin;
+#endif
   // large u64 batches of an interleaved section without a select directory
   // (no Rice column: IC-C) take the shared-table kernel; Rice selects keep
   // the many-CTA kernel, whose occupancy hides their scan latency better
-  if (keys64 && !mono && !dsel && n < ((int64_t)1 << 32) && sh <= (size_t)optin &&
+  if (keys64 && !mono && !dsel && n < ((int64_t)1 << 32) && (c32 || sh <= (size_t)optin) &&
       nq >= (int64_t)num_sms() * 4096 && (reinterpret_cast<uintptr_t>(keys64) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-    PHB_CUDA_TRY(cudaFuncSetAttribute(k_query_enc_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      optin));
-    note_launch(), k_query_enc_s<<<num_sms(), 1024, sh, st>>>(
-        reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, key_off,
-        entries, bcount, section, c, dsel, dstride, reinterpret_cast<longlong2*>(out));
+    if (c32) {
+      PHB_CUDA_TRY(cudaFuncSetAttribute(k_query_enc_s<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      note_launch(), k_query_enc_s<true><<<num_sms(), 1024, sh32, st>>>(
+          reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, key_off,
+          entries, bcount, section, c, dsel, dstride, reinterpret_cast<longlong2*>(out));
+    } else {
+      PHB_CUDA_TRY(cudaFuncSetAttribute(k_query_enc_s<false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      note_launch(), k_query_enc_s<false><<<num_sms(), 1024, sh, st>>>(
+          reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, key_off,
+          entries, bcount, section, c, dsel, dstride, reinterpret_cast<longlong2*>(out));
+    }
   } else if (keys64)
     note_launch(), k_query_enc<0><<<g, 256, 0, st>>>(buf, offsets, keys64, nq, seed, n, (uint64_t)nparts, key_off,
                                       entries, bcount, section, c, mono, dsel, dstride, out);
