@@ -24,7 +24,7 @@ key_off = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
 deltas = torch.empty(nparts + 1, dtype=torch.int64, device=dev)
 stats = torch.empty(2, dtype=torch.int64, device=dev)
 _native.check(L.phb_layout(P(counts), nparts, 0, 0, n, nparts, P(key_off), P(deltas), P(stats), st), "l")
-cur = torch.empty(nparts * 16, dtype=torch.int32, device=dev)
+cur = torch.empty(nparts * 32, dtype=torch.int32, device=dev)  # room for strided-cursor variants
 lo = torch.empty(2 * n, dtype=torch.int64, device=dev)  # room for 16-byte record variants
 bid = torch.empty(n, dtype=torch.int16, device=dev)
 ts = []
