@@ -597,11 +597,14 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     if constexpr (G > 1) {
       // closed form of the sequential loop: seeds before the first group with
       // a valid displacement self-collided (k trials) or swept m (k*m)
-      uint32_t collg = 0;
-#pragma unroll
-      for (int gi = 0; gi < G; ++gi) collg |= (uint32_t)(((cball >> (gi * L)) & LMASK) != 0) << gi;
+      // one bit per self-collided group, without a loop of compares (-1.7%)
+      uint32_t collg;
+      if constexpr (G == 4)
+        collg = ((__vcmpne4(cball, 0u) & 0x01010101u) * 0x01020408u) >> 24;
+      else
+        collg = (uint32_t)((cball & 0xffffu) != 0u) | ((uint32_t)((cball >> 16) != 0u) << 1);
       const int src = __ffs(fball) - 1;  // first lane with a valid d lies in the first found group
-      const int gw = src < 0 ? G : src / L;
+      const int gw = fball ? (int)((uint32_t)src / (uint32_t)L) : G;
       const int ncoll = __popc(collg & ((1u << gw) - 1u));
       // k <= 16, m <= 3072, gw <= 4: every term fits 32 bits
       const uint32_t tr = k * ((uint32_t)ncoll + m * (uint32_t)(gw - ncoll));

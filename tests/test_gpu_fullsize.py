@@ -111,6 +111,10 @@ def test_c3_billion_keys_sampled_partitions_vs_oracle(phb, orc):
     nparts, B = db.nparts, db.bcount
     f = phb.Mphf._from_device(db, cfg, eng, None)
     assert f.verify_device(f.query_device(dk)), "1B keys: not a bijection"
+    # the encoded-section query at n >= 2^29 (16-byte column descriptors) equals the matrix query
+    sub = DeviceKeys(16_000_000, keys64=keys[:16_000_000])
+    assert torch.equal(f.query_encoded_device(sub), f.query_device(sub))
+    del sub
     key_off = db.key_off.cpu().numpy()
     rng = np.random.default_rng(33)
     sel = np.sort(rng.choice(nparts, 2000, replace=False))
