@@ -19,22 +19,25 @@
 //    bucket sizes / offsets, the processing order and the current bucket's
 //    base positions. Keys stay in L1/L2 (bucket-grouped scratch `glo`).
 //  * Displacement search is bit-parallel: valid(d) = AND_i free(p_i + d).
-//    Lane l owns the three consecutive 32-bit words [3l, 3l+3) of the valid
-//    mask (96 words = 3072 displacements per pass, conflict-free since 3 is
-//    odd), i.e. 4 shared loads + 3 funnel shifts per key; a ballot + ffs
-//    picks the smallest d. Every 4 keys the warp stops early once all
-//    words are saturated.
-//  * Small buckets test G seeds per step (G = 4 for k <= 8, 2 for k <= 16),
-//    one lane group per seed; the batched instantiations are lean (seeds
-//    >= 1 below the cap, closed-form resolution), the single-seed one keeps
+//    A lane owns consecutive 32-bit words of the valid mask (single-seed
+//    steps: 3 words per lane, 96 words = 3072 displacements per pass); keys
+//    are swept in pairs, both windows OR-ed into the accumulator with one
+//    3-input LOP3 per word (2 funnel shifts + 1 LOP3 per pair-word); a
+//    ballot + ffs picks the smallest d. Single- and 2-seed steps stop early
+//    once every word of every group is saturated.
+//  * Small buckets test G seeds per step (G = 4 for k <= 8 with 88-word
+//    windows, 2 for k <= 16 with 96-word windows), one lane group per seed;
+//    the batched instantiations are lean (seeds >= 1 below the cap,
+//    closed-form resolution in 32-bit arithmetic), the single-seed one keeps
 //    seed 0's duplicate check and the cap. Per-seed hashes of the first 4096
 //    seeds come from a compile-time table.
 //  * Self-collision of a candidate s: __match_any_sync on positions for
 //    k <= 32, shared-memory atomicOr test-and-set for larger buckets.
 //  * Trials use the closed form k * (S_self + sum_fail(dmax+1) + d* + 1),
 //    identical to the reference's per-candidate counting.
-//  * Bound: SM issue / ALU pipe (funnel shift + OR per window word), not HBM
-//    (profiles/search_sm_c2.json); measured alternatives in DESIGN.md §3.
+//  * Bound: SM issue (74%), with the shared LSU (78%) and the ALU pipe (68%)
+//    next, not HBM (profiles/search_sm_c2.json); measured alternatives in
+//    DESIGN.md §3.
 #include <cstdio>
 #include "common.cuh"
 #include "phobic_internal.h"
@@ -42,10 +45,8 @@
 namespace phb {
 
 // Register budget: CTAs of 4 warps per SM (8 -> 64 registers, 32 warps/SM).
-// Variants measured slower at C2 (round 1, tools/variant_bench.py) and
-// removed: 64/128-bit window loads, key pairs folded with 3-input ORs,
-// IMAD.WIDE funnel shifts, closed-form batch resolution, conflict-free
-// multi-seed layout, out-of-line generic path, no G = 2 batches.
+// Variants measured at C2 (tools/variant_bench.py) are listed with their
+// times in DESIGN.md §3.
 #ifndef PHB_MINB
 #define PHB_MINB 8
 #endif
