@@ -939,7 +939,7 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
         continue;
       }
 #ifndef PHB_MB_E
-#define PHB_MB_E 4.0f
+#define PHB_MB_E 2.0f  // C2 lambda = 5 search 7.22 -> 6.99 ms (4.0: the round-2a gate)
 #endif
       // expected seed-0 fits of this bucket, m (1 - fill)^k: the step pays
       // when the first (largest) bucket almost surely fits at seed 0
