@@ -77,6 +77,10 @@ __device__ __forceinline__ uint64_t seed_hash(int64_t s) {
 #define PHB_W2 96
 #endif
 constexpr int W4 = PHB_W4, W2 = PHB_W2;
+#ifndef PHB_PRO_D
+#define PHB_PRO_D 4  // prologue records in flight per lane
+#endif
+constexpr int PRO_D = PHB_PRO_D;
 #ifndef PHB_G1_E100  // seed-0 batch gate: expected seed-0 fits x 100 (0 = off)
 #define PHB_G1_E100 0
 #endif
@@ -863,9 +867,24 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     // records: separate (lo, u16 bucket id) arrays, or 16-byte (lo, bucket id)
     // records when bid is null (phb_scatter's one-store layout)
     const uint64_t* const rec = a.bid ? nullptr : a.lo;
+    // PRO_D records per lane in flight: the loads come straight from K3's
+    // writes (L2 / DRAM); one at a time they serialised the prologue
+    // (C2 search: lambda = 4 7.48 -> 7.12 ms, lambda = 5 6.96 -> 6.77 ms)
+    {
+      uint32_t q = lane;
 #pragma unroll 1
-    for (uint32_t q = lane; q < m; q += 32)
-      atomicAdd(&smem[cnt + (rec ? (uint32_t)rec[2 * (kb + q) + 1] : (uint32_t)a.bid[kb + q])], 1u);
+      for (; q + 32 * (PRO_D - 1) < m; q += 32 * PRO_D) {
+        uint32_t bb[PRO_D];
+#pragma unroll
+        for (int e = 0; e < PRO_D; ++e)
+          bb[e] = rec ? (uint32_t)__ldcg(&rec[2 * (kb + q + 32 * e) + 1]) : (uint32_t)a.bid[kb + q + 32 * e];
+#pragma unroll
+        for (int e = 0; e < PRO_D; ++e) atomicAdd(&smem[cnt + bb[e]], 1u);
+      }
+#pragma unroll 1
+      for (; q < m; q += 32)
+        atomicAdd(&smem[cnt + (rec ? (uint32_t)rec[2 * (kb + q) + 1] : (uint32_t)a.bid[kb + q])], 1u);
+    }
     __syncwarp();
     uint32_t run = 0, maxsz = 0;
 #pragma unroll 1
@@ -879,20 +898,36 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     }
     maxsz = warp_max(maxsz);
     __syncwarp();
-#pragma unroll 1
-    for (uint32_t q = lane; q < m; q += 32) {
-      uint64_t lo;
-      uint32_t b;
+    {
+      uint32_t q = lane;
       if (rec) {
-        const ulonglong2 r = reinterpret_cast<const ulonglong2*>(rec)[kb + q];
-        lo = r.x;
-        b = (uint32_t)r.y;
-      } else {
-        lo = a.lo[kb + q];
-        b = a.bid[kb + q];
+#pragma unroll 1
+        for (; q + 32 * (PRO_D - 1) < m; q += 32 * PRO_D) {
+          ulonglong2 r[PRO_D];
+#pragma unroll
+          for (int e = 0; e < PRO_D; ++e) r[e] = reinterpret_cast<const ulonglong2*>(rec)[kb + q + 32 * e];
+#pragma unroll
+          for (int e = 0; e < PRO_D; ++e) {
+            const uint32_t at = atomicAdd(&smem[endp + (uint32_t)r[e].y], 1u);
+            a.glo[kb + at] = r[e].x;
+          }
+        }
       }
-      const uint32_t at = atomicAdd(&smem[endp + b], 1u);
-      a.glo[kb + at] = lo;
+#pragma unroll 1
+      for (; q < m; q += 32) {
+        uint64_t lo;
+        uint32_t b;
+        if (rec) {
+          const ulonglong2 r = reinterpret_cast<const ulonglong2*>(rec)[kb + q];
+          lo = r.x;
+          b = (uint32_t)r.y;
+        } else {
+          lo = a.lo[kb + q];
+          b = a.bid[kb + q];
+        }
+        const uint32_t at = atomicAdd(&smem[endp + b], 1u);
+        a.glo[kb + at] = lo;
+      }
     }
     const uint32_t occ_used = min((uint32_t)plan.occ_w, (2 * m) / 32 + 104);
 #pragma unroll 1
