@@ -86,7 +86,10 @@ constexpr int PRO_D = PHB_PRO_D;
 #endif
 constexpr int SH = 256;     // size classes of the counting-sort bucket order
 constexpr int PMAX = 256;   // bucket sizes whose base positions are staged in smem
-constexpr int WARPS = 4;    // warps (= partitions in flight) per CTA
+#ifndef PHB_WARPS
+#define PHB_WARPS 4
+#endif
+constexpr int WARPS = PHB_WARPS;  // warps (= partitions in flight) per CTA
 constexpr unsigned FULL = 0xffffffffu;
 
 // Per-warp shared-memory plan, in 32-bit words.
@@ -459,13 +462,21 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   const uint64_t key = act ? kl[gl] : 0ull;
   uint16_t* const mypos = pos16 + grp * L;
   const uint32_t wb = (uint32_t)gl * WPL;
+#ifdef PHB_PEND
+  // (s_next + G) m, kept incrementally: the guard compares without a multiply
+  int64_t pend = (s_next + G) * (int64_t)m;
+#endif
 #pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
     if constexpr (G > 1) {
+#ifdef PHB_PEND
+      if ((s_next < 1 && !allow0) || pend - 1 > cap) return {0, trials, -1};
+#else
       // batches never see the seed cap, and seed 0 only when allowed (it
       // is handed back below if it self-collides): those go to the
       // single-seed instantiation, which keeps the seed-by-seed resolution
       if ((s_next < 1 && !allow0) || (s_next + G) * (int64_t)m - 1 > cap) return {0, trials, -1};
+#endif
     }
     STAT(G == 1 ? 0 : (G == 2 ? 1 : 2), 1);
     const int64_t s = s_next + grp;
@@ -549,9 +560,10 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         xb = yb;
       }
       // every 4 keys, when keys remain: stop once every window is saturated
-      // (not at G = 4: k <= 8 buckets almost never saturate all four groups
-      // before their last pair, so the check only costs issue slots)
-      if (G < 4 && (i & 2u) && i + 2 < k) {
+      // (single-seed steps only: k <= 16 buckets almost never saturate every
+      // group of a 2- or 4-seed batch before their last pair, so there the
+      // check only costs issue slots; measured -2% and -1%)
+      if (G == 1 && (i & 2u) && i + 2 < k) {
         uint32_t all = FULL;
 #pragma unroll
         for (int t = 0; t < WPL; ++t) all &= acc[t];
@@ -625,6 +637,9 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
       }
       trials += (int64_t)tr;
       s_next += G;
+#ifdef PHB_PEND
+      pend += G * (int64_t)m;
+#endif
       __syncwarp();
     } else {
       // single-seed step (G = 1): seed 0's duplicate check and the seed cap
