@@ -462,21 +462,13 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   const uint64_t key = act ? kl[gl] : 0ull;
   uint16_t* const mypos = pos16 + grp * L;
   const uint32_t wb = (uint32_t)gl * WPL;
-#ifdef PHB_PEND
-  // (s_next + G) m, kept incrementally: the guard compares without a multiply
-  int64_t pend = (s_next + G) * (int64_t)m;
-#endif
 #pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
     if constexpr (G > 1) {
-#ifdef PHB_PEND
-      if ((s_next < 1 && !allow0) || pend - 1 > cap) return {0, trials, -1};
-#else
       // batches never see the seed cap, and seed 0 only when allowed (it
       // is handed back below if it self-collides): those go to the
       // single-seed instantiation, which keeps the seed-by-seed resolution
       if ((s_next < 1 && !allow0) || (s_next + G) * (int64_t)m - 1 > cap) return {0, trials, -1};
-#endif
     }
     STAT(G == 1 ? 0 : (G == 2 ? 1 : 2), 1);
     const int64_t s = s_next + grp;
@@ -637,9 +629,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
       }
       trials += (int64_t)tr;
       s_next += G;
-#ifdef PHB_PEND
-      pend += G * (int64_t)m;
-#endif
       __syncwarp();
     } else {
       // single-seed step (G = 1): seed 0's duplicate check and the seed cap
