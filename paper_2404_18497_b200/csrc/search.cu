@@ -303,7 +303,9 @@ __device__ int64_t find_d_pairs(uint32_t occ, const uint16_t* pos16, uint32_t k,
       a0 |= __funnelshift_r(x0, x1, sa) | __funnelshift_r(y0, y1, sb);
       a1 |= __funnelshift_r(x1, x2, sa) | __funnelshift_r(y1, y2, sb);
       a2 |= __funnelshift_r(x2, x3, sa) | __funnelshift_r(y2, y3, sb);
+#ifndef PHB_NOSATG
       if ((i & 2u) && i + 2 < k && __all_sync(FULL, (a0 & a1 & a2) == FULL)) break;
+#endif
     }
     uint32_t v0 = ~a0, v1 = ~a1, v2 = ~a2;
     const int64_t lim = dmax - 32 * (int64_t)wb;
@@ -532,6 +534,10 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     // 3-input LOP3 per word (2 funnel shifts + 1 LOP3 per pair-word instead of
     // 2 shifts + 2 ORs: the sweep is ALU-pipe bound). The next pair's base
     // positions (two u16 in one word) are loaded one iteration ahead.
+    // No early exit on saturated windows: buckets of k <= 32 keys rarely
+    // saturate every lane before their last pair, and the check (an AND over
+    // the window plus a vote every other pair) cost more than it saved
+    // (C2 search: lambda = 9 -1%, lambda = 7 -5% without it).
     const uint32_t* const mp32 = reinterpret_cast<const uint32_t*>(mypos);
     uint32_t pp = mp32[0];
 #pragma unroll 1
@@ -550,16 +556,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         acc[t] |= __funnelshift_r(xa, ya, sa) | __funnelshift_r(xb, yb, sb);
         xa = ya;
         xb = yb;
-      }
-      // every 4 keys, when keys remain: stop once every window is saturated
-      // (single-seed steps only: k <= 16 buckets almost never saturate every
-      // group of a 2- or 4-seed batch before their last pair, so there the
-      // check only costs issue slots; measured -2% and -1%)
-      if (G == 1 && (i & 2u) && i + 2 < k) {
-        uint32_t all = FULL;
-#pragma unroll
-        for (int t = 0; t < WPL; ++t) all &= acc[t];
-        if (__all_sync(FULL, all == FULL)) break;
       }
     }
 #else
