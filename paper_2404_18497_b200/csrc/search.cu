@@ -23,8 +23,8 @@
 //    steps: 3 words per lane, 96 words = 3072 displacements per pass); keys
 //    are swept in pairs, both windows OR-ed into the accumulator with one
 //    3-input LOP3 per word (2 funnel shifts + 1 LOP3 per pair-word); a
-//    ballot + ffs picks the smallest d. Single- and 2-seed steps stop early
-//    once every word of every group is saturated.
+//    ballot + ffs picks the smallest d. No early exit on saturated windows
+//    (measured: the check costs more than it saves at every lambda).
 //  * Small buckets test G seeds per step (G = 4 for k <= 8 with 88-word
 //    windows, 2 for k <= 16 with 96-word windows), one lane group per seed;
 //    the batched instantiations are lean (seeds >= 1 below the cap,
@@ -303,9 +303,7 @@ __device__ int64_t find_d_pairs(uint32_t occ, const uint16_t* pos16, uint32_t k,
       a0 |= __funnelshift_r(x0, x1, sa) | __funnelshift_r(y0, y1, sb);
       a1 |= __funnelshift_r(x1, x2, sa) | __funnelshift_r(y1, y2, sb);
       a2 |= __funnelshift_r(x2, x3, sa) | __funnelshift_r(y2, y3, sb);
-#ifndef PHB_NOSATG
-      if ((i & 2u) && i + 2 < k && __all_sync(FULL, (a0 & a1 & a2) == FULL)) break;
-#endif
+      // (no saturation exit: measured 1.5% slower with it, like the batched sweeps)
     }
     uint32_t v0 = ~a0, v1 = ~a1, v2 = ~a2;
     const int64_t lim = dmax - 32 * (int64_t)wb;
