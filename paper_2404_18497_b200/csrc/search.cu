@@ -81,9 +81,6 @@ constexpr int W4 = PHB_W4, W2 = PHB_W2;
 #define PHB_PRO_D 4  // prologue records in flight per lane
 #endif
 constexpr int PRO_D = PHB_PRO_D;
-#ifndef PHB_G1_E100  // seed-0 batch gate: expected seed-0 fits x 100 (0 = off)
-#define PHB_G1_E100 0
-#endif
 constexpr int SH = 256;     // size classes of the counting-sort bucket order
 constexpr int PMAX = 256;   // bucket sizes whose base positions are staged in smem
 #ifndef PHB_WARPS
@@ -453,7 +450,7 @@ template <int G, int W = 96>
 __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos16, uint32_t k,
                                      const uint64_t* kl, uint32_t m, int64_t cap,
                                      int64_t& s_next, int64_t trials, int max_batches,
-                                     int lane, bool allow0 = false) {
+                                     int lane) {
   constexpr int L = 32 / G, WPL = W / L;  // W: window words per seed (W >= (m + 31) / 32)
   static_assert(W % L == 0 && W <= 96, "window");
   constexpr uint32_t LMASK = L == 32 ? FULL : ((1u << L) - 1u);
@@ -465,10 +462,10 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
 #pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
     if constexpr (G > 1) {
-      // batches never see the seed cap, and seed 0 only when allowed (it
-      // is handed back below if it self-collides): those go to the
+      // batches never see seed 0 or the seed cap: those go to the
       // single-seed instantiation, which keeps the seed-by-seed resolution
-      if ((s_next < 1 && !allow0) || (s_next + G) * (int64_t)m - 1 > cap) return {0, trials, -1};
+      // (a gate that let batches start at seed 0 measured 9% slower)
+      if (s_next < 1 || (s_next + G) * (int64_t)m - 1 > cap) return {0, trials, -1};
     }
     STAT(G == 1 ? 0 : (G == 2 ? 1 : 2), 1);
     const int64_t s = s_next + grp;
@@ -478,9 +475,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     // every lane must execute the vote (no short-circuit around it)
     const uint32_t tpeers = __match_any_sync(FULL, tag);
     const uint32_t cball = __ballot_sync(FULL, act && __popc(tpeers) > 1);
-    // seed 0 self-collides: only the single-seed step checks for duplicate
-    // keys (_kernels.py:312-319); nothing consumed, the caller takes it there
-    if (G > 1 && allow0 && s_next == 0 && (cball & LMASK)) return {0, trials, -1};
     if (act) mypos[gl] = (uint16_t)p;
 #ifndef PHB_NOPAIR
     // keys are swept in pairs: an odd k repeats its last key (OR is idempotent)
@@ -1013,23 +1007,16 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
         // kernel's instruction footprint small
         int64_t s_next = 0;
         const uint32_t kg1 = 16u;  // larger buckets stay single-seed
-        int first = k > kg1 ? (1 << 30) : 1;
-#if PHB_G1_E100 > 0
-        // seed 0 unlikely to fit (expected seed-0 fits m (1 - fill)^k below
-        // PHB_G1_E100 / 100): no single-seed step, the first batch takes seed 0
-        if (k <= kg1 && (float)m * __powf((float)(m - placed) / (float)m, (float)k) <
-                            0.01f * (float)PHB_G1_E100)
-          first = 0;
-#endif
-        res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, 0, first, lane);
+        res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, 0, k > kg1 ? (1 << 30) : 1,
+                              lane);
         if (res.status < 0) {
           // batched instantiations hold 32 / G lanes per seed: only k <= 16
           if (k <= 8 && (W4 >= 96 || m <= 32u * W4))
             res = small_bucket<4, W4>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
-                                      lane, s_next == 0);
+                                      lane);
           else if (k <= kg1 && (W2 >= 96 || m <= 32u * W2))
             res = small_bucket<2, W2>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
-                                      lane, s_next == 0);
+                                      lane);
           // near the seed cap, or k > 16: single-seed steps until decided
           while (res.status < 0)
             res = small_bucket<1>(occ, dmask, pos16, k, kl, m, cap, s_next, res.trials, 1 << 30,
