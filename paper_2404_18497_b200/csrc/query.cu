@@ -158,11 +158,26 @@ __global__ void __launch_bounds__(256)
 #ifndef PHB_Q_NK
 #define PHB_Q_NK 4
 #endif
+// Byte-key master hashes as (hi, lo) pairs, for the two-pass string query.
+__global__ void __launch_bounds__(256) k_hash_pairs(const uint8_t* __restrict__ buf,
+                                                    const int64_t* __restrict__ offsets, int64_t n,
+                                                    uint64_t seed, ulonglong2* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = __ldg(offsets + i), b = __ldg(offsets + i + 1);
+    const Hash128 h = murmur3_bytes(buf + a, b - a, seed);
+    out[i] = make_ulonglong2(h.hi, h.lo);
+  }
+}
+
 // Seed hashes mix64(s ^ POSITION_SALT) of seeds s < QGT_N, for the
 // encoded-section kernel's shared table (K7es); the matrix kernel K7s keeps
 // the 64-bit mix (a table there measured 3% slower).
 constexpr int QGT_N = 256;
 
+// HASHED: keys2 holds (hi, lo) master-hash pairs (byte keys, hashed by
+// k_hash_pairs first) instead of u64 keys.
+template <bool HASHED>
 __global__ void __launch_bounds__(1024, 1)
     k_query32s_u64x4(const ulonglong2* __restrict__ keys2, int64_t nq, uint64_t seed, int64_t n,
                      uint64_t nparts, const int64_t* __restrict__ key_off,
@@ -179,19 +194,25 @@ __global__ void __launch_bounds__(1024, 1)
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
        v += (int64_t)gridDim.x * blockDim.x) {
     uint64_t k[NK];
+    ulonglong2 hk[HASHED ? NK : 1];
+    if (HASHED) {
 #pragma unroll
-    for (int e = 0; e < NK / 2; ++e) {
-      // streaming keys / outputs are marked evict-first so the seed table stays in L2
-      const ulonglong2 kv = __ldcs(keys2 + (NK / 2) * v + e);
-      k[2 * e] = kv.x;
-      k[2 * e + 1] = kv.y;
+      for (int e = 0; e < NK; ++e) hk[e] = __ldcs(keys2 + NK * v + e);
+    } else {
+#pragma unroll
+      for (int e = 0; e < NK / 2; ++e) {
+        // streaming keys / outputs are marked evict-first so the seed table stays in L2
+        const ulonglong2 kv = __ldcs(keys2 + (NK / 2) * v + e);
+        k[2 * e] = kv.x;
+        k[2 * e + 1] = kv.y;
+      }
     }
     uint64_t lo[NK];
     uint2 pe[NK];
     uint32_t p[NK];
 #pragma unroll
     for (int e = 0; e < NK; ++e) {
-      const Hash128 h = murmur3_u64(k[e], seed);
+      const Hash128 h = HASHED ? Hash128{hk[e].x, hk[e].y} : murmur3_u64(k[e], seed);
       lo[e] = h.lo;
       const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
       const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
@@ -206,7 +227,8 @@ __global__ void __launch_bounds__(1024, 1)
   }
   const int64_t t = nv * NK + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t < nq) {
-    const Hash128 h = murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
+    const Hash128 h = HASHED ? Hash128{__ldg(keys2 + t).x, __ldg(keys2 + t).y}
+                             : murmur3_u64(__ldg(reinterpret_cast<const uint64_t*>(keys2) + t), seed);
     const uint32_t j = (uint32_t)mulhi(h.hi, nparts);
     const uint32_t b = bucket_of_pairs(tab, h.hi, bcount);
     const uint32_t pp = __ldg(seeds32 + (int64_t)(b - 1) * (int64_t)nparts + j);
@@ -608,9 +630,9 @@ int launch_query32(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
     if (key_off && sh <= (size_t)optin && nq >= (int64_t)num_sms() * 4096) {
       // the largest shared footprint this path takes (concurrent launches
       // from other host threads must not see a lower cap)
-      PHB_CUDA_TRY(cudaFuncSetAttribute(k_query32s_u64x4,
+      PHB_CUDA_TRY(cudaFuncSetAttribute(k_query32s_u64x4<false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-      note_launch(), k_query32s_u64x4<<<num_sms(), 1024, sh, st>>>(
+      note_launch(), k_query32s_u64x4<false><<<num_sms(), 1024, sh, st>>>(
           reinterpret_cast<const ulonglong2*>(keys64), nq, seed, n, (uint64_t)nparts, key_off,
           entries, bcount, seeds32, reinterpret_cast<longlong2*>(out));
     } else {
@@ -619,6 +641,36 @@ int launch_query32(const uint8_t* buf, const int64_t* offsets, const uint64_t* k
           entries, bcount, seeds32, reinterpret_cast<longlong2*>(out));
     }
   } else {
+    // large batches: hash all keys first (the fused kernel's per-thread byte
+    // loads thrash L1/L2 next to the seed gathers: 8.9 GB of DRAM reads for
+    // 5.5 GB of key bytes at C5), then the shared-table query over the hashes
+    const size_t sh = sizeof(double2) * BUCKET_TAB + sizeof(uint32_t) * (size_t)(nparts + 1);
+    int dev = 0, optin = 0;
+    PHB_CUDA_TRY(cudaGetDevice(&dev));
+    PHB_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+#ifndef PHB_NO_Q2PASS
+    if (key_off && sh <= (size_t)optin && nq >= (int64_t)num_sms() * 4096 &&
+        (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+      // chunks of QCH keys: a pooled 512 MB scratch (the pool keeps 1 GB)
+      constexpr int64_t QCH = 32ll << 20;
+      const int64_t ch = nq < QCH ? nq : QCH;
+      ulonglong2* hp = nullptr;
+      PHB_CUDA_TRY(scratch_alloc(reinterpret_cast<void**>(&hp), sizeof(ulonglong2) * (size_t)ch, st));
+      PHB_CUDA_TRY(cudaFuncSetAttribute(k_query32s_u64x4<true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      for (int64_t c0 = 0; c0 < nq; c0 += ch) {
+        const int64_t c = nq - c0 < ch ? nq - c0 : ch;
+        note_launch(), k_hash_pairs<<<qgrid(c), 256, 0, st>>>(buf, offsets + c0, c, seed, hp);
+        PHB_CUDA_TRY(cudaGetLastError());
+        note_launch(), k_query32s_u64x4<true><<<num_sms(), 1024, sh, st>>>(
+            hp, c, seed, n, (uint64_t)nparts, key_off, entries, bcount, seeds32,
+            reinterpret_cast<longlong2*>(out + c0));
+        PHB_CUDA_TRY(cudaGetLastError());
+      }
+      PHB_CUDA_TRY(cudaFreeAsync(hp, st));
+      return 0;
+    }
+#endif
     note_launch(), k_query32_bytes<<<qgrid(nq), 256, 0, st>>>(buf, offsets, nq, seed, n,
                                                               (uint64_t)nparts, part2, entries,
                                                               bcount, seeds32, out);

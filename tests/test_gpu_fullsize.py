@@ -94,6 +94,15 @@ def test_c5_strings_full_size_vs_oracle(phb, orc):
     idx = np.random.default_rng(3).choice(n, 200_000, replace=False)
     assert _query_sample_equal(f, ref, orc, None, idx, corpus=(buf, off))
     assert f.is_bijection_on(corpus)
+    # the batched device query of all 100M keys (hash pass + shared-table
+    # query, in 32M-key chunks) agrees with the oracle on the sample
+    full = f.query_many(corpus)
+    lens = off[idx + 1] - off[idx]
+    soff = np.zeros(len(idx) + 1, np.int64)
+    np.cumsum(lens, out=soff[1:])
+    sbuf = np.concatenate([buf[off[i]:off[i + 1]] for i in idx])
+    hi, lo = orc.murmur3_many(sbuf, soff, f.global_seed)
+    assert np.array_equal(full[idx], ref.query_hashes(hi, lo))
 
 
 def test_c3_billion_keys_sampled_partitions_vs_oracle(phb, orc):
