@@ -239,7 +239,17 @@ def reference_build(sample_keys: int, threads: int, offset: int = 0):
     t0 = time.perf_counter()
     f = ph.build(corpus, cfg)
     dt = time.perf_counter() - t0
+    # the reference's batched query of the same sample (Mphf.query_many,
+    # mphf.py:130-145: single-threaded numba), beside the GPU query metric
+    f.query_many(ph.KeyCorpus(keys[:1000].view(np.uint8).copy(),
+                              np.arange(0, 8 * 1000 + 1, 8, dtype=np.int64)))  # JIT warm-up
+    tq = time.perf_counter()
+    f.query_many(corpus)
+    dq = time.perf_counter() - tq
     return {"value": sample_keys / dt, "unit": "keys/s", "cores": threads, "kind": "reference",
+            "query": {"value": sample_keys / dq / 1e6, "unit": "Mq/s", "cores": 1,
+                      "what": "pilothash Mphf.query_many of the sample (single-threaded, as the "
+                              "reference ships it)"},
             "impl": "pilothash 0.1.0 build() (numba kernels), baseline/_ref",
             "trials_per_s": f.stats.trials_total / dt,
             "sample": f"{sample_keys:,} keys of the same synthetic stream (8-byte LE strings), "
