@@ -680,6 +680,17 @@ def run_gpu(args):
                  "what": "instruction floor / measured instructions x issue-active "
                          "(ncu --set full of the same workload)",
                  "source": "profiles/search_sm_c2.json"}
+        if sm.get("shared_wavefronts"):
+            # the shared-memory pipe (the fullest one): one conflict-free
+            # wavefront per 32 lanes x 32 candidates per key is the floor
+            wpk = sm["shared_wavefronts"] / sm.get("n_keys", 1e8)
+            floor_wf = trials_per_key / 1024.0
+            issue["shared_lsu"] = {
+                "wavefronts_per_key": round(wpk, 1), "floor_wavefronts_per_key": round(floor_wf, 1),
+                "bank_conflict_share": round(sm.get("shared_bank_conflicts", 0.0)
+                                             / sm["shared_wavefronts"], 3),
+                "frac": round(floor_wf / wpk * sm["lsu_shared_wavefront_pct_elapsed"] / 100.0, 4),
+                "what": "wavefront floor / measured shared wavefronts x shared-pipe utilisation"}
     q_gbs = n_local * QUERY_BYTES / (q_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world,
