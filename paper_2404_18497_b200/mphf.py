@@ -390,7 +390,7 @@ class Mphf:
                 seeds = self.seeds.device_matrix()  # decoded once from the device body
             return self._dev_key_off, self._dev_entries, seeds
         if self._dev_key_off is None:
-            d = torch.from_numpy(np.ascontiguousarray(self.layout.deltas, np.int64)).to(dev)
+            d = torch.from_numpy(np.array(self.layout.deltas, np.int64)).to(dev)  # (a writable copy)
             key_off = torch.empty(self.layout.num_partitions + 1, dtype=torch.int64, device=dev)
             _native.call("phb_offsets_from_deltas", _native.ptr(d), self.n,
                          self.layout.num_partitions, _native.ptr(key_off), _native.stream())

@@ -21,6 +21,12 @@ big = np.unique(rng.integers(0, 2**64, size=1_000_000, dtype=np.uint64))
 f = phb.build(big, phb.BuildConfig(lambda_=4.0, partition_size=100.0, encoder="ic-c"))
 db = torch.from_numpy(big.view(np.int64)).cuda()
 assert f.verify_device(f.query_device(db))
+# the encoded-section shared-table query (8-byte column descriptors, seed-hash table)
+assert torch.equal(f.query_encoded_device(db), f.query_device(db))
+# string keys: the batched query in two passes (hash pairs, shared-table query)
+scorpus = phb.gen_keys(650_000, 11)
+fs = phb.build(scorpus, phb.BuildConfig(lambda_=8.0, partition_size=2500.0, encoder="ic-r"))
+assert fs.is_bijection_on(scorpus)
 corpus = phb.gen_keys(5000, 3)
 f = phb.build(corpus, phb.BuildConfig(lambda_=8.0, partition_size=500.0))
 assert f.is_bijection_on(corpus)
