@@ -476,10 +476,8 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     const uint32_t tpeers = __match_any_sync(FULL, tag);
     const uint32_t cball = __ballot_sync(FULL, act && __popc(tpeers) > 1);
     if (act) mypos[gl] = (uint16_t)p;
-#ifndef PHB_NOPAIR
     // keys are swept in pairs: an odd k repeats its last key (OR is idempotent)
     if ((k & 1u) && (uint32_t)gl == k - 1) mypos[k] = (uint16_t)p;
-#endif
     __syncwarp();
     const bool gcoll = ((cball >> (grp * L)) & LMASK) != 0;
     const int64_t pbase = s * (int64_t)m;
@@ -521,7 +519,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         acc[t] = (dead_group || lt < 0) ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
       }
     }
-#ifndef PHB_NOPAIR
     // Keys in pairs: both windows are OR-ed into the accumulator with one
     // 3-input LOP3 per word (2 funnel shifts + 1 LOP3 per pair-word instead of
     // 2 shifts + 2 ORs: the sweep is ALU-pipe bound). The next pair's base
@@ -550,32 +547,6 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         xb = yb;
       }
     }
-#else
-    // the next key's base position is loaded one iteration ahead, so its
-    // shared-memory latency hides behind the current key's window loads
-    uint32_t pnext = mypos[0];
-#pragma unroll 1
-    for (uint32_t i = 0; i < k; ++i) {
-      STAT(3, 1);
-      const uint32_t pi = pnext;
-      pnext = mypos[i + 1 < k ? i + 1 : i];
-      const uint32_t sh = pi & 31;
-      const uint32_t W = occ + (pi >> 5) + wb;
-      uint32_t x = smem[W];
-#pragma unroll
-      for (int t = 0; t < WPL; ++t) {
-        const uint32_t y = smem[W + t + 1];
-        acc[t] |= __funnelshift_r(x, y, sh);
-        x = y;
-      }
-      if ((i & 3) == 3) {
-        uint32_t all = FULL;
-#pragma unroll
-        for (int t = 0; t < WPL; ++t) all &= acc[t];
-        if (__all_sync(FULL, all == FULL)) break;
-      }
-    }
-#endif
     // this lane's first valid displacement (d <= dmax), or -1
     uint32_t sat = FULL;
 #pragma unroll
