@@ -350,3 +350,29 @@ def test_pinned_chunked_build_equals_device_build(phb):
     torch.cuda.synchronize()
     ref = BuildEngine(cfg).run(phb.keygen.to_device(dev_keys, dev_keys.device), 0)
     assert torch.equal(res.blob[57:res.total_bytes], ref.blob[57:ref.total_bytes])
+
+
+def test_long_and_mixed_length_keys_vs_oracle(phb, orc):
+    """Byte keys from 0 B to 6 KB (many murmur3 blocks, every alignment in
+    the flat buffer) against the oracle: bytes, trials and queries, through
+    both the per-thread and the batched (two-pass, >= 606k keys) query."""
+    rng = np.random.default_rng(4242)
+    n = 700_000
+    lens = rng.integers(0, 64, size=n)
+    long_idx = rng.choice(n, 300, replace=False)
+    lens[long_idx] = rng.integers(64, 6001, size=300)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    buf = rng.integers(0, 256, size=int(off[-1]), dtype=np.uint8)
+    uniq = sorted({bytes(buf[off[i]:off[i + 1]]) for i in range(n)})
+    corpus = phb.KeyCorpus.from_keys(uniq)
+    cfg = phb.BuildConfig(lambda_=7.0, partition_size=2500.0, encoder="ic-r")
+    f = phb.build(corpus, cfg)
+    ref = orc.build((corpus.buf, corpus.offsets), lambda_=7.0, P=2500.0, encoder="ic-r")
+    assert f.serialize() == ref.serialize()
+    assert f.stats.trials_total == int(ref.trials.sum())
+    hi, lo = orc.murmur3_many(corpus.buf, corpus.offsets, f.global_seed)
+    want = ref.query_hashes(hi, lo)
+    assert np.array_equal(f.query_many(corpus), want)            # batched (two-pass) path
+    sub = phb.KeyCorpus.from_keys(uniq[:5000])
+    assert np.array_equal(f.query_many(sub), want[:5000])        # per-thread path
