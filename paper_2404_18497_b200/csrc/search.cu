@@ -643,7 +643,10 @@ __device__ uint32_t multi_bucket0(const SearchArgs& a, int64_t row, uint32_t occ
                                   uint16_t* pos16, const uint16_t* order, uint32_t oi, uint32_t nG,
                                   uint32_t cnt, uint32_t endp, const uint64_t* kbase, uint32_t m,
                                   uint64_t g0, int64_t& tr_out, uint32_t& placed, int lane) {
-  constexpr int L = 8, WPL = 12;
+#ifndef PHB_MB_WPL
+#define PHB_MB_WPL 11  // 88-word windows like the 4-seed batches (lambda = 5: -1.6%)
+#endif
+  constexpr int L = 8, WPL = PHB_MB_WPL;  // 8 lanes x WPL words of the seed-0 window
   const int grp = lane >> 3, gl = lane & 7;
   const bool ing = (uint32_t)grp < nG;
   const uint32_t bg = ing ? order[oi + grp] : 0u;
@@ -918,7 +921,7 @@ __global__ void __launch_bounds__(WARPS * 32, PHB_MINB) k_search(SearchArgs a, S
     // speculative seed-0 steps over several small buckets pay while most of
     // them fit at seed 0, i.e. below ~85% fill; they need the whole seed-0
     // displacement range below the cap
-    const bool multi_ok = small_ok && cap >= (int64_t)m - 1;
+    const bool multi_ok = small_ok && cap >= (int64_t)m - 1 && m <= 32u * 8u * PHB_MB_WPL;
     uint32_t placed = 0, mb_fail = 0xffffffffu;
 #pragma unroll 1
     for (uint32_t oi = 0; oi < nb;) {
