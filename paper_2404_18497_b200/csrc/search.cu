@@ -698,30 +698,35 @@ __device__ uint32_t multi_bucket0(const SearchArgs& a, int64_t row, uint32_t occ
       if (acc[t] != FULL) tw = (uint32_t)t, vv = acc[t];
     myd = 32u * (wb + tw) + (uint32_t)(__ffs(~vv) - 1);
   }
-  uint32_t accepted = 0;
-#pragma unroll 1
-  for (uint32_t g = 0; g < nG; ++g) {
-    const uint32_t gb = (fball >> (g * L)) & 0xffu;
-    if (!gb) break;  // no fit at seed 0, or a self-collision: the regular path decides
-    const uint32_t d = __shfl_sync(FULL, myd, (int)(g * L) + __ffs(gb) - 1);
-    uint32_t slot = p + d;
-    if (slot >= m) slot -= m;
-    const bool mine = (uint32_t)grp == g && act;
-    const bool taken = mine && ((smem[occ + (slot >> 5)] >> (slot & 31)) & 1u);
-    if (__any_sync(FULL, taken)) break;  // collides with a group placed in this step
-    if (mine) mark(occ, slot, m, 500 + (int)kg);
-    __syncwarp();
-    const uint32_t kgg = __shfl_sync(FULL, kg, (int)(g * L));
-    const uint32_t bgg = __shfl_sync(FULL, bg, (int)(g * L));
-    const int64_t tr = (int64_t)kgg * ((int64_t)d + 1);
-    if (lane == 0) {
-      a.seeds[row * a.s_sj + (int64_t)(bgg - 1) * a.s_sb] = (uint64_t)d;
-      if (a.trials) a.trials[row * a.s_sj + (int64_t)(bgg - 1) * a.s_sb] = tr;
-    }
-    tr_out += tr;
-    placed += kgg;
-    ++accepted;
+  // Acceptance of all groups at once: a group's first fit (free before the
+  // step) stands unless one of its slots equals a slot of an earlier group of
+  // this step (match on the slots); the step accepts groups 0 .. A-1, A the
+  // first group without a fit or with such a repeat. (A group-by-group loop
+  // of shuffles, shared reads and votes cost 7-13% of the low-lambda search.)
+  const uint32_t gbm = (fball >> (grp * L)) & 0xffu;
+  const uint32_t dm = __shfl_sync(FULL, myd, gbm ? grp * L + __ffs(gbm) - 1 : lane);
+  const bool cand = act && gbm != 0u;
+  uint32_t slot = p + dm;
+  if (slot >= m) slot -= m;
+  const uint32_t stag = cand ? slot : (0x80000000u | (uint32_t)lane);
+  const uint32_t speers = __match_any_sync(FULL, stag);
+  const bool rep = cand && (speers & ((1u << (grp * L)) - 1u)) != 0u;  // an earlier group's slot
+  const uint32_t repb = __ballot_sync(FULL, rep);
+  uint32_t stopg = 0;  // groups that stop the step: no fit, or a repeat
+#pragma unroll
+  for (uint32_t g = 0; g < 4; ++g)
+    if (g < nG && (((fball >> (g * L)) & 0xffu) == 0u || ((repb >> (g * L)) & 0xffu) != 0u))
+      stopg |= 1u << g;
+  const uint32_t accepted = stopg ? (uint32_t)(__ffs(stopg) - 1) : nG;
+  const bool acc_g = (uint32_t)grp < accepted;
+  if (acc_g && act) mark(occ, slot, m, 500 + (int)kg);
+  const int64_t trg = acc_g && gl == 0 ? (int64_t)kg * ((int64_t)dm + 1) : 0;
+  if (acc_g && gl == 0) {
+    a.seeds[row * a.s_sj + (int64_t)(bg - 1) * a.s_sb] = (uint64_t)dm;
+    if (a.trials) a.trials[row * a.s_sj + (int64_t)(bg - 1) * a.s_sb] = trg;
   }
+  tr_out += (int64_t)__reduce_add_sync(FULL, (uint32_t)trg);
+  placed += __reduce_add_sync(FULL, acc_g && gl == 0 ? kg : 0u);
   __syncwarp();  // the sweep's reads of the base positions precede the next writer's
   return accepted;
 }
