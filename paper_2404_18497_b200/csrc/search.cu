@@ -98,11 +98,11 @@ __host__ __device__ inline SmemPlan smem_plan(int64_t m_max, uint32_t bcount) {
   SmemPlan p;
   // reads reach word (m-1)/32 + 3*31 + 3 of a pass, marks reach bit 2m - 1
   p.occ_w = (int)((2 * m_max) / 32 + 104);
-  p.scr_w = (int)(m_max / 32 + 2);
+  p.scr_w = (int)((m_max / 32 + 3) & ~1);  // even: 8-byte aligned sweep entries follow
   p.cnt_w = (int)bcount + 1;  // cnt and endp each
   p.ord_w = (int)(bcount + 2) / 2;
   p.sh_w = SH;       // shist + srun as u16
-  p.pos_w = PMAX / 2;  // u16 base positions
+  p.pos_w = PMAX / 2;  // u16 base positions (generic) or u32 sweep entries (k <= 32)
   p.occ_w = (p.occ_w + 3) & ~3;  // keep the mask table that follows 16-byte aligned
   // the bucket-order scratch (shist/srun) is dead before the search state
   // (mask table, collision map, positions) is written: they share one region
@@ -434,6 +434,34 @@ __device__ BucketResult generic_bucket(uint32_t occ, uint32_t scr, uint16_t* pos
   }
 }
 
+// A key's sweep entry (u32, in the position area): bits 0-4 the funnel shift
+// p & 31 (SHF.R.W reads only those bits), bits 7 and up the byte offset of
+// its first bitmap word, 4 (p >> 5), shifted left by 5. The word address is
+// then one LEA.HI off the lane's base and the shift needs no mask; a pair of
+// entries is one LDS.64 (C2 search 22.1 -> 21.7 ms: 5 fewer instructions per
+// key pair against u16 base positions).
+__device__ __forceinline__ uint32_t sweep_entry(uint32_t p) { return ((p >> 5) << 7) | (p & 31u); }
+
+// One pair of keys OR-ed into a lane's WPL accumulator words: word t gets
+// funnel(occ[r + wb + t], occ[r + wb + t + 1], p & 31) of both keys
+// (r = p >> 5, ob = the byte address of occ[wb]). Keys in pairs: both windows
+// go into the accumulator with one 3-input LOP3 per word (2 funnel shifts +
+// 1 LOP3 per pair-word instead of 2 shifts + 2 ORs).
+template <int WPL>
+__device__ __forceinline__ void sweep_pair(uint32_t (&acc)[WPL], const char* ob, uint32_t ea,
+                                           uint32_t eb) {
+  const uint32_t* const Wa = reinterpret_cast<const uint32_t*>(ob + (ea >> 5));
+  const uint32_t* const Wb = reinterpret_cast<const uint32_t*>(ob + (eb >> 5));
+  uint32_t xa = Wa[0], xb = Wb[0];
+#pragma unroll
+  for (int t = 0; t < WPL; ++t) {
+    const uint32_t ya = Wa[t + 1], yb = Wb[t + 1];
+    acc[t] |= __funnelshift_r(xa, ya, ea) | __funnelshift_r(xb, yb, eb);
+    xa = ya;
+    xb = yb;
+  }
+}
+
 // Batched search for small buckets (k <= 32 / G) in partitions with
 // m <= 3072: G consecutive seeds s are tested per step, one group of
 // L = 32 / G lanes per seed, each lane owning WPL = 96 / L consecutive
@@ -457,8 +485,9 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
   const int grp = lane / L, gl = lane % L;
   const bool act = (uint32_t)gl < k;
   const uint64_t key = act ? kl[gl] : 0ull;
-  uint16_t* const mypos = pos16 + grp * L;
+  uint32_t* const mye = reinterpret_cast<uint32_t*>(pos16) + grp * L;  // sweep entries
   const uint32_t wb = (uint32_t)gl * WPL;
+  const char* const ob = reinterpret_cast<const char*>(smem + occ + wb);
 #pragma unroll 1
   for (int bt = 0; bt < max_batches; ++bt) {
     if constexpr (G > 1) {
@@ -475,9 +504,9 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
     // every lane must execute the vote (no short-circuit around it)
     const uint32_t tpeers = __match_any_sync(FULL, tag);
     const uint32_t cball = __ballot_sync(FULL, act && __popc(tpeers) > 1);
-    if (act) mypos[gl] = (uint16_t)p;
+    if (act) mye[gl] = sweep_entry(p);
     // keys are swept in pairs: an odd k repeats its last key (OR is idempotent)
-    if ((k & 1u) && (uint32_t)gl == k - 1) mypos[k] = (uint16_t)p;
+    if ((k & 1u) && (uint32_t)gl == k - 1) mye[k] = sweep_entry(p);
     __syncwarp();
     const bool gcoll = ((cball >> (grp * L)) & LMASK) != 0;
     const int64_t pbase = s * (int64_t)m;
@@ -519,33 +548,22 @@ __device__ BucketResult small_bucket(uint32_t occ, uint32_t dmask, uint16_t* pos
         acc[t] = (dead_group || lt < 0) ? FULL : (lt < 31 ? ~((2u << lt) - 1u) : 0u);
       }
     }
-    // Keys in pairs: both windows are OR-ed into the accumulator with one
-    // 3-input LOP3 per word (2 funnel shifts + 1 LOP3 per pair-word instead of
-    // 2 shifts + 2 ORs: the sweep is ALU-pipe bound). The next pair's base
-    // positions (two u16 in one word) are loaded one iteration ahead.
+    // Keys in pairs (sweep_pair); the next pair's entries are loaded one
+    // iteration ahead.
     // No early exit on saturated windows: buckets of k <= 32 keys rarely
     // saturate every lane before their last pair, and the check (an AND over
     // the window plus a vote every other pair) cost more than it saved
     // (C2 search: lambda = 9 -1%, lambda = 7 -5% without it).
-    const uint32_t* const mp32 = reinterpret_cast<const uint32_t*>(mypos);
-    uint32_t pp = mp32[0];
+    const uint2* const me2 = reinterpret_cast<const uint2*>(mye);
+    uint2 ee = me2[0];
 #pragma unroll 1
     for (uint32_t i = 0; i < k; i += 2) {
       STAT(3, 2);
-      const uint32_t pa = pp & 0xffffu, pb = pp >> 16;
-      // the next pair's positions; past the last pair this reads a spare
-      // entry of the (256-entry) position area, never used
-      pp = mp32[(i >> 1) + 1];
-      const uint32_t sa = pa & 31, sb = pb & 31;
-      const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
-      uint32_t xa = smem[Wa], xb = smem[Wb];
-#pragma unroll
-      for (int t = 0; t < WPL; ++t) {
-        const uint32_t ya = smem[Wa + t + 1], yb = smem[Wb + t + 1];
-        acc[t] |= __funnelshift_r(xa, ya, sa) | __funnelshift_r(xb, yb, sb);
-        xa = ya;
-        xb = yb;
-      }
+      const uint32_t ea = ee.x, eb = ee.y;
+      // the next pair's entries; past the last pair this reads a spare
+      // entry of the (128-entry) position area, never used
+      ee = me2[(i >> 1) + 1];
+      sweep_pair<WPL>(acc, ob, ea, eb);
     }
     // this lane's first valid displacement (d <= dmax), or -1
     uint32_t sat = FULL;
@@ -662,28 +680,19 @@ __device__ uint32_t multi_bucket0(const SearchArgs& a, int64_t row, uint32_t occ
   const uint32_t kpad = (kmax + 1u) & ~1u;
   const uint32_t from = kg ? (uint32_t)(grp * L) + min((uint32_t)gl, kg - 1u) : (uint32_t)lane;
   const uint32_t pfill = __shfl_sync(FULL, p, from);
-  uint16_t* const mypos = pos16 + grp * L;
-  if ((uint32_t)gl < kpad) mypos[gl] = (uint16_t)pfill;
+  uint32_t* const mye = reinterpret_cast<uint32_t*>(pos16) + grp * L;  // sweep entries
+  if ((uint32_t)gl < kpad) mye[gl] = sweep_entry(pfill);
   __syncwarp();
   const uint32_t wb = (uint32_t)gl * WPL;
   uint32_t acc[WPL];
 #pragma unroll
   for (int t = 0; t < WPL; ++t) acc[t] = smem[dmask + wb + t];
-  const uint32_t* const mp32 = reinterpret_cast<const uint32_t*>(mypos);
+  const uint2* const me2 = reinterpret_cast<const uint2*>(mye);
+  const char* const ob = reinterpret_cast<const char*>(smem + occ + wb);
 #pragma unroll 1
   for (uint32_t i = 0; i < kpad; i += 2) {
-    const uint32_t pp = mp32[i >> 1];
-    const uint32_t pa = pp & 0xffffu, pb = pp >> 16;
-    const uint32_t sa = pa & 31, sb = pb & 31;
-    const uint32_t Wa = occ + (pa >> 5) + wb, Wb = occ + (pb >> 5) + wb;
-    uint32_t xa = smem[Wa], xb = smem[Wb];
-#pragma unroll
-    for (int t = 0; t < WPL; ++t) {
-      const uint32_t ya = smem[Wa + t + 1], yb = smem[Wb + t + 1];
-      acc[t] |= __funnelshift_r(xa, ya, sa) | __funnelshift_r(xb, yb, sb);
-      xa = ya;
-      xb = yb;
-    }
+    const uint2 ee = me2[i >> 1];
+    sweep_pair<WPL>(acc, ob, ee.x, ee.y);
   }
   uint32_t sat = FULL;
 #pragma unroll
